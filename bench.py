@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Bench: frames/s and Gaussians/s of the B200 rasterizer at 1080p (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2]
+
+A step renders one 1920x1080 frame of the C2 scene (G(1M, seed 2), SH degree 3,
+fitted poly-1 kernel with opacity-aware culling) through ps_render with the scene
+resident in HBM. Under torchrun (N > 1) every rank renders its own orbit view of
+a replicated scene (view sharding, no data-path collective; "scaling": "weak");
+timing is CUDA events on the rasterizer's stream, barrier + max over ranks.
+`--impl reference` times the reference's own CPU renderer (oracle/_ref, the
+unmodified reference library built from source) on the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/s and Gaussians/s at 1080p, poly-1 vs exp, 1/2/4/8 B200 vs CPU ref"
+
+WORKLOADS = {
+    # name: (scene kind, seed, n, width, height, views)
+    "c1": ("g", 1, 10_000, 256, 256, 1),
+    "c2": ("g", 2, 1_000_000, 1920, 1080, 256),
+    "c3": ("g", 4, 6_000_000, 3840, 2160, 1),
+    "c4": ("g", 5, 3_000_000, 1920, 1080, 256),
+    "c5": ("skewed", 3, 1_000_000, 1920, 1080, 1),
+}
+HEADLINE = ("poly1/opacity", "poly1", "OpacityAware")
+COMPARE = [("exp/stp", "exp", "StopThePop"), ("poly1/zero", "poly1", "ZeroCrossing"),
+           ("poly2p/opacity", "poly2p", "OpacityAware"), ("poly3/opacity", "poly3", "OpacityAware")]
+# FP32 lane-instructions per kernel evaluation / per blended fragment
+OPS_PER_EVAL = {"poly1": 6, "poly2p": 8, "poly3": 8, "exp": 7, "poly2": 8}
+OPS_PER_BLEND = 6
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_cfg(api, kname: str, mode: str, sh_degree: int):
+    return api.RasterConfig(kernel=api.fitted_kernel(kname), culling_mode=getattr(api.CullingMode, mode),
+                            sh_degree=sh_degree)
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle  # the reference's own CPU renderer (oracle/_ref)
+    from paper_2603_18707_b200 import api
+
+    kind, seed, n, w, h, _ = WORKLOADS[args.workload]
+    ref = oracle.Reference()
+    splats, deg = api.synthetic_splat3d({"g": 3, "skewed": 4}[kind], seed, n)
+    cam = api.orbit_cameras(256, w, h)[0].to_struct()
+    cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg).to_struct()
+    for _ in range(args.warmup):
+        ref.render(splats, cam, cfg)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.render(splats, cam, cfg)
+        times.append(time.perf_counter() - t0)
+    ms = 1000.0 * sum(times) / len(times)
+    fps = 1000.0 / ms
+    cores = ref.resolve_thread_count(0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.workload),
+        "gaussians_per_s": fps * n,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} full frames of {args.workload} ({HEADLINE[0]}) via "
+                                   "polysplat::render, OpenMP over all host threads"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(name: str) -> dict:
+    kind, seed, n, w, h, views = WORKLOADS[name]
+    return {"workload": f"{name.upper()}: synthetic G({n}, seed {seed}{', skewed opacity' if kind == 'skewed' else ''}), "
+                        f"{w}x{h}, SH degree 3, {HEADLINE[0]} (fitted poly-1, opacity-aware bound)",
+            "gaussians": n, "width": w, "height": h, "kernel": HEADLINE[0], "parallelism": "view-sharded",
+            "l2": "flushed between timed steps (256 MiB write); scene (280 MB) also exceeds the 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_2603_18707_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    kind, seed, n, w, h, nviews = WORKLOADS[args.workload]
+    scene = api.Scene.synthetic(kind, seed, n)
+    deg = scene.sh_degree
+    cams = api.orbit_cameras(nviews, w, h)
+    view = (rank * max(1, nviews // max(world, 1))) % nviews
+    cam = cams[view]
+    r = api.Rasterizer(local)
+    ds = r.upload(scene)
+    lib = api.lib()
+    import ctypes as C
+    stream = torch.cuda.ExternalStream(lib.ps_ctx_stream(r.handle), device=torch.device("cuda", local))
+    out_rgb = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+    out_t = torch.empty((h, w), dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    cam_s = cam.to_struct()
+
+    def render_dev(cfg_s):
+        st = lib.ps_render(r.handle, ds.handle, C.byref(cam_s), C.byref(cfg_s), out_rgb.data_ptr(),
+                           out_t.data_ptr(), 1, None)
+        if st != 0:
+            raise RuntimeError(api.last_error(r.handle))
+
+    def timed(cfg_s, steps, warmup, sample_clocks=False):
+        for _ in range(warmup):
+            render_dev(cfg_s)
+        r.set_timing(True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        stage_sum = {}
+        launches = 0
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local) if sample_clocks else None
+        if sampler:
+            sampler.__enter__()
+        for k in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            evs[k][0].record(stream)
+            render_dev(cfg_s)
+            evs[k][1].record(stream)
+            s = r.stats()
+            launches += s["kernel_launches"]
+            for key, v in s["stage_ms"].items():
+                stage_sum[key] = stage_sum.get(key, 0.0) + v
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__(None, None, None)
+        r.set_timing(False)
+        ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        stages = {k: v / steps for k, v in stage_sum.items()}
+        return ms, stages, launches, (sampler.summary() if sampler else None)
+
+    cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg)
+    cfg_s = cfg.to_struct()
+    ms, stages, launches, clocks = timed(cfg_s, args.steps, args.warmup, sample_clocks=True)
+    fps = world * 1000.0 / ms
+
+    # work counters of the timed frame (untimed render with counters)
+    fb_unused, ctr = r.render(ds, cam, cfg, counters=True)
+    st = r.stats()
+    result = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+              "vs_baseline": None, "dtype": "f32 blend, f64 preprocess/binning", "data": "synthetic",
+              "config": workload_config(args.workload), "gaussians_per_s": fps * n,
+              "gpu_launches": launches, "clocks": clocks}
+    result["config"]["view_per_rank"] = "orbit view (rank * 256/N)"
+    result["stages_ms"] = stages
+    result["work"] = {"visible": st["visible"], "pairs": st["pairs"], "kernel_evaluations": ctr.kernel_evaluations,
+                      "fragments_blended": ctr.fragments_blended, "replay_pixels": st["replay_pixels"],
+                      "exact_alpha_evals": st["exact_alpha_evals"]}
+
+    if rank == 0:
+        result["roofline"], result["roofline_stages"] = roofline(r, stages, n, deg, st, ctr, HEADLINE[1])
+
+    # poly-vs-exp and the rest of the kernel matrix (fewer steps each)
+    if not args.no_compare:
+        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms}}
+        for label, kname, mode in COMPARE:
+            c2 = make_cfg(api, kname, mode, deg).to_struct()
+            m2, _, _, _ = timed(c2, max(3, min(args.steps, 10)), 3)
+            kern[label] = {"frames_per_s": 1000.0 / m2, "ms": m2}
+        result["kernels"] = kern
+        result["poly1_vs_exp_speedup"] = kern["exp/stp"]["ms"] / kern[HEADLINE[0]]["ms"]
+
+    # end to end through the public API with host buffers: H2D of the scene
+    # from pinned memory + render + D2H of the image, every step
+    if not args.no_e2e:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(scene, k))).pin_memory()
+               for k in ("means", "scales", "rotations", "opacities", "sh")}
+        h_rgb = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+        h_t = torch.empty((h, w), dtype=torch.float32).pin_memory()
+        ke = max(3, min(args.steps, 10))
+        for it in range(2 + ke):
+            if it == 2:
+                if dist:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            stt = lib.ps_scene_update_soa(r.handle, ds.handle, pin["means"].data_ptr(), pin["scales"].data_ptr(),
+                                          pin["rotations"].data_ptr(), pin["opacities"].data_ptr(),
+                                          pin["sh"].data_ptr(), 0)
+            assert stt == 0, api.last_error(r.handle)
+            stt = lib.ps_render(r.handle, ds.handle, C.byref(cam_s), C.byref(cfg_s), h_rgb.data_ptr(),
+                                h_t.data_ptr(), 0, None)
+            assert stt == 0, api.last_error(r.handle)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ke
+        if dist:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = sum(v.numel() * v.element_size() for v in pin.values())
+        result["e2e"] = {"value": world * 1000.0 / ems, "unit": "frames/s", "ms_per_step": ems,
+                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h * w * 16),
+                         "path": "ps_scene_update_soa (pinned host SoA) + ps_render (host outputs)"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args.workload)
+
+    ds.close()
+    r.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
+    """Per-stage achieved vs peak; the dominant stage goes to the top-level `roofline`."""
+    import ctypes as C
+
+    from paper_2603_18707_b200 import api
+
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    tf = C.c_double(0)
+    api._check(api.lib().ps_measure_fp32_peak(r.handle, C.byref(tf)), r.handle)
+    fp32_tflops = tf.value
+    v, p = st["visible"], st["pairs"]
+    E, B = ctr.kernel_evaluations, ctr.fragments_blended
+    sh_bytes = 12 * (deg + 1) ** 2
+    work = {  # SURVEY §8(d) algorithmic work per stage
+        "preprocess": ("hbm", n * (88 + sh_bytes) + v * 64),
+        "depth_sort": ("hbm", v * 12 * 2),
+        "duplicate": ("hbm", p * 12),
+        "tile_sort": ("hbm", p * 12 * 2),
+        "ranges": ("hbm", p * 8),
+        "blend": ("fp32", OPS_PER_EVAL.get(kname, 8) * E + OPS_PER_BLEND * B),
+    }
+    out = {}
+    for name, (bound, amount) in work.items():
+        ms = stages.get(name, 0.0)
+        if ms <= 0:
+            continue
+        if bound == "hbm":
+            ach = amount / (ms * 1e-3) / 1e9
+            out[name] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "algorithmic": amount, "ms": ms}
+        else:
+            ach = amount / (ms * 1e-3) / 1e12           # tera FP32 lane-instructions / s
+            peak = fp32_tflops / 2.0                     # FFMA = 1 lane-instruction = 2 flops
+            out[name] = {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "Tinst/s", "frac": ach / peak,
+                         "algorithmic": amount, "ms": ms,
+                         "peak_source": f"measured FFMA microbenchmark {fp32_tflops:.1f} TFLOP/s"}
+    dom = max(out, key=lambda k: out[k]["ms"]) if out else None
+    top = dict(out[dom]) if dom else {}
+    if dom:
+        top["kernel"] = dom
+        top["traffic"] = None
+        top["peak_note"] = ("HBM peak from MEASURED_PEAKS.json" if top["bound"] == "hbm"
+                            else "FP32 issue peak measured in-run (no FP32 entry in MEASURED_PEAKS.json)")
+    return top, out
+
+
+def cpu_baseline(workload: str) -> dict:
+    """The reference's own renderer (oracle/_ref) on this host, bounded sample."""
+    try:
+        from oracle import oracle
+        from paper_2603_18707_b200 import api
+        kind, seed, n, w, h, _ = WORKLOADS[workload]
+        ref = oracle.Reference()
+        splats, deg = api.synthetic_splat3d({"g": 3, "skewed": 4}[kind], seed, n)
+        cam = api.orbit_cameras(256, w, h)[0].to_struct()
+        cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg).to_struct()
+        ref.render(splats, cam, cfg)  # warm-up
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref.render(splats, cam, cfg)
+            ts.append(time.perf_counter() - t0)
+        ms = 1000.0 * statistics.median(ts)
+        return {"value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0), "kind": "reference",
+                "ms_per_frame": ms, "sample": f"median of 3 full {workload.upper()} frames ({HEADLINE[0]}), "
+                                               "polysplat::render built from the reference sources, all host threads"}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "frames/s", "cores": None, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default="c2")
+    ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,262 @@
+// blend.cu — K6: front-to-back alpha blending per tile (raster.cpp:227-301).
+//
+// One CTA per tile, one pixel per thread (tile_size^2 <= 1024). The tile's
+// splat list is staged through shared memory in batches of blockDim records
+// (gathered by splat index from the fp32 blend records written by K1, with the
+// fp64 mean turned into tile-local fp32 coordinates on the way in).
+//
+// Per (pixel, splat) the fast path is
+//     u = (dx + beta dy);  q = A u^2 + gamma dy^2;  skip unless q <= q_hi
+// i.e. the reference's alpha < epsilon test (raster.cpp:269-271) moved into
+// quadric space: for a kernel non-increasing in q, min(.999, o k(q)) >= eps
+// <=> q <= q*(o). No MUFU on the skip path for any kernel; polynomial kernels
+// evaluate alpha with FFMA only. q in [q_lo, q_hi] (the certified fp32 error
+// band) is re-decided with the reference's fp64 arithmetic (exact_alpha_ge_eps).
+// The transmittance test (raster.cpp:272-277) carries a per-pixel relative
+// error bound eT; a pixel whose T lands inside the band around the floor is
+// flagged and replayed exactly in fp64 by K7. Early termination: the CTA stops
+// when no pixel is live (__syncthreads_count), the reference's `remaining == 0`.
+#include "kernels.h"
+
+namespace ps {
+
+namespace {
+
+struct BlendArgs {
+    FrameParams P;
+    const uint2* ranges;
+    const uint32_t* pval;
+    const double2* mean2d;
+    const float4* bl0;
+    const float4* bl1;
+    const float2* bl2;
+    const double2* conic_ab;
+    const double2* conic_cq;
+    const double* opacity_eff;
+    uint32_t* flags;
+    DevCounters* ctr;
+    float* out_rgb;
+    float* out_t;
+};
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// Blend kernel in fp64 for the exact decisions (set per frame, stream-ordered).
+__constant__ ps_kernel c_exact_kernel;
+__constant__ double c_exact_eps;
+
+// eval_kernel (kernel.cpp:162-172) with explicitly rounded ops (never contracted)
+__device__ double eval_kernel_rn(double x) {
+    const ps_kernel& k = c_exact_kernel;
+    if (k.kind == PS_KERNEL_EXPONENTIAL) return exp(dmul(-0.5, x));
+    double p = k.coeffs[k.order];
+    for (int i = k.order - 1; i >= 0; --i) p = dadd(dmul(p, x), k.coeffs[i]);
+    if (k.kind == PS_KERNEL_POLY_RELU) return (p < 0.0) ? 0.0 : p;
+    return x < k.first_root ? p : 0.0;
+}
+
+// The reference's alpha decision for pixel (gx, gy) and splat i, in its exact
+// fp64 arithmetic (raster.cpp:262-271): dx = px + 0.5 - mx, q = a dx dx +
+// 2 b dx dy + c dy dy, alpha = min(0.999, o k(q)); returns !(alpha < eps).
+__device__ __noinline__ bool exact_alpha_ge_eps(const double2* __restrict__ mean2d,
+                                                const double2* __restrict__ conic_ab,
+                                                const double2* __restrict__ conic_cq,
+                                                const double* __restrict__ opacity_eff, uint32_t i,
+                                                int gx, int gy) {
+    const double2 m = mean2d[i];
+    const double2 ab = conic_ab[i];
+    const double2 cq = conic_cq[i];
+    const double o = opacity_eff[i];
+    const double dx = dsub(dadd(static_cast<double>(gx), 0.5), m.x);
+    const double dy = dsub(dadd(static_cast<double>(gy), 0.5), m.y);
+    const double q = dadd(dadd(dmul(dmul(ab.x, dx), dx), dmul(dmul(dmul(2.0, ab.y), dx), dy)),
+                          dmul(dmul(cq.x, dy), dy));
+    const double v = dmul(o, eval_kernel_rn(q));
+    const double alpha = (v < 0.999) ? v : 0.999;
+    return !(alpha < c_exact_eps);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// fp32 alpha of an accepted fragment. KIND 0: exponential (oval = log2 o);
+// KIND 1: polynomial (oval = o), relu/piecewise semantics.
+template <int KIND>
+__device__ __forceinline__ float alpha_f32(float q, float oval, const KernelF32& kf) {
+    if (KIND == 0) {
+        return fminf(0.999f, ex2_approx(fmaf(q, -0.72134752044448170f, oval)));
+    } else {
+        float p = kf.c[kf.order];
+        for (int j = kf.order - 1; j >= 0; --j) p = fmaf(p, q, kf.c[j]);
+        if (kf.kind == PS_KERNEL_POLY_PIECEWISE && !(q < kf.first_root)) p = 0.0f;
+        return fminf(0.999f, fmaxf(oval * p, 0.0f));
+    }
+}
+
+template <int KIND, int MODE, bool COUNT>
+__global__ void k_blend(const BlendArgs A) {
+    extern __shared__ float4 smem[];
+    const int nt = blockDim.x;
+    float4* s0 = smem;
+    float4* s1 = s0 + nt;
+    float4* s2 = s1 + nt;
+    uint32_t* si = reinterpret_cast<uint32_t*>(s2 + nt);
+
+    const FrameParams& P = A.P;
+    const int tile = blockIdx.x;
+    const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
+    const int ts = P.cfg.tile_size;
+    const int W = P.cam.width, H = P.cam.height;
+    const int px0 = tx * ts, py0 = ty * ts;
+    const int t = threadIdx.x;
+    const int lx = t % ts, ly = t / ts;
+    const int gx = px0 + lx, gy = py0 + ly;
+    const bool inside = (t < ts * ts) && gx < W && gy < H;
+    const float xc = lx + 0.5f, yc = ly + 0.5f;
+    const float eps = P.eps_f, floor_f = P.floor_f;
+
+    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, eT = 0.0f;
+    bool done = !inside, flagged = false;
+    uint32_t term = 0xffffffffu, nbl = 0, nexact = 0;
+
+    const uint2 range = A.ranges[tile];
+    const int L = static_cast<int>(range.y - range.x);
+    for (int base = 0; base < L; base += nt) {
+        if (__syncthreads_count(!done) == 0) break;
+        const int j = base + t;
+        if (j < L) {
+            const uint32_t i = A.pval[range.x + j];
+            const double2 m = A.mean2d[i];
+            const float4 b0 = A.bl0[i];
+            const float4 b1 = A.bl1[i];
+            const float2 b2 = A.bl2[i];
+            s0[t] = make_float4(static_cast<float>(m.x - px0), static_cast<float>(m.y - py0), b0.x, b0.y);
+            s1[t] = make_float4(b0.z, b0.w, b1.x, b1.y);
+            s2[t] = make_float4(b1.z, b1.w, b2.x, b2.y);
+            si[t] = i;
+        }
+        __syncthreads();
+        const int cnt = min(nt, L - base);
+        if (!done) {
+            for (int k = 0; k < cnt; ++k) {
+                const float4 v0 = s0[k];
+                const float4 v1 = s1[k];
+                const float dx = xc - v0.x, dy = yc - v0.y;
+                const float u = fmaf(v0.w, dy, dx);
+                const float q = fmaf(v0.z * u, u, v1.x * dy * dy);
+                float alpha;
+                if (MODE == kQuadricThreshold) {
+                    if (!(q <= v1.y)) continue; // alpha < eps certainly (or pixel/splat pair skipped)
+                    if (q >= v1.z) {            // inside the fp32 error band: decide in fp64
+                        ++nexact;
+                        if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                    }
+                    alpha = alpha_f32<KIND>(q, v1.w, P.kf);
+                } else {
+                    alpha = alpha_f32<KIND>(q, v1.w, P.kf);
+                    if (alpha < eps - v1.y) continue;
+                    if (alpha < eps + v1.y) {
+                        ++nexact;
+                        if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                    }
+                }
+                const float4 v2 = s2[k];
+                eT += v2.x;
+                const float test_t = fmaf(-T, alpha, T);
+                if (test_t < fmaf(floor_f, eT, floor_f)) {
+                    done = true;
+                    if (test_t < fmaf(-floor_f, eT, floor_f)) term = static_cast<uint32_t>(base + k);
+                    else flagged = true;
+                    break;
+                }
+                const float w = alpha * T;
+                cr = fmaf(v2.y, w, cr);
+                cg = fmaf(v2.z, w, cg);
+                cb = fmaf(v2.w, w, cb);
+                T = test_t;
+                ++nbl;
+            }
+        }
+    }
+
+    if (inside) {
+        const size_t pix = static_cast<size_t>(gy) * W + gx;
+        A.out_rgb[3 * pix + 0] = cr;
+        A.out_rgb[3 * pix + 1] = cg;
+        A.out_rgb[3 * pix + 2] = cb;
+        A.out_t[pix] = T;
+        if (flagged) {
+            const unsigned long long slot = atomicAdd(&A.ctr->replay_px, 1ull);
+            A.flags[slot] = static_cast<uint32_t>(pix);
+        }
+    }
+    // per-CTA sums of the reference's counters (raster.cpp:268,283); flagged
+    // pixels are counted by the exact replay instead
+    unsigned long long ev = 0, bl = 0;
+    if (COUNT && inside && !flagged) {
+        ev = term != 0xffffffffu ? term + 1u : static_cast<unsigned>(L);
+        bl = nbl;
+    }
+    unsigned long long ex = nexact;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ev += __shfl_xor_sync(0xffffffffu, ev, o);
+        bl += __shfl_xor_sync(0xffffffffu, bl, o);
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+    }
+    if ((t & 31) == 0) {
+        if (ev) atomicAdd(&A.ctr->evals, ev);
+        if (bl) atomicAdd(&A.ctr->blended, bl);
+        if (ex) atomicAdd(&A.ctr->exact_evals, ex);
+    }
+}
+
+template <int KIND, int MODE>
+void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, cudaStream_t st) {
+    if (count) k_blend<KIND, MODE, true><<<n_tiles, nt, smem, st>>>(a);
+    else k_blend<KIND, MODE, false><<<n_tiles, nt, smem, st>>>(a);
+}
+
+} // namespace
+
+int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, DevCounters* ctr,
+                 BlendOut out, bool count_work, cudaStream_t st) {
+    BlendArgs a;
+    a.P = P;
+    a.ranges = f.ranges;
+    a.pval = pair_vals;
+    a.mean2d = f.mean2d;
+    a.bl0 = f.bl0;
+    a.bl1 = f.bl1;
+    a.bl2 = f.bl2;
+    a.conic_ab = f.conic_ab;
+    a.conic_cq = f.conic_cq;
+    a.opacity_eff = f.opacity_eff;
+    a.flags = f.flags;
+    a.ctr = ctr;
+    a.out_rgb = out.rgb;
+    a.out_t = out.t;
+    const int ts = P.cfg.tile_size;
+    const int nt = ((ts * ts + 31) / 32) * 32;
+    const size_t smem = static_cast<size_t>(nt) * (3 * sizeof(float4) + sizeof(uint32_t));
+    const int n_tiles = P.tiles_x * P.tiles_y;
+    if (n_tiles == 0) return 0;
+    cudaMemcpyToSymbolAsync(c_exact_kernel, &P.cfg.kernel, sizeof(ps_kernel), 0, cudaMemcpyHostToDevice, st);
+    cudaMemcpyToSymbolAsync(c_exact_eps, &P.cfg.epsilon, sizeof(double), 0, cudaMemcpyHostToDevice, st);
+    const bool expk = P.kf.kind == PS_KERNEL_EXPONENTIAL;
+    if (P.threshold_mode == kQuadricThreshold) {
+        if (expk) launch_t<0, kQuadricThreshold>(a, n_tiles, nt, smem, count_work, st);
+        else launch_t<1, kQuadricThreshold>(a, n_tiles, nt, smem, count_work, st);
+    } else {
+        if (expk) launch_t<0, kAlphaThreshold>(a, n_tiles, nt, smem, count_work, st);
+        else launch_t<1, kAlphaThreshold>(a, n_tiles, nt, smem, count_work, st);
+    }
+    return 1;
+}
+
+} // namespace ps

@@ -1,0 +1,108 @@
+// common.cuh — device data layout shared by the rasterizer stages.
+//
+// HBM layout (all arrays indexed by the ORIGINAL splat index i unless noted):
+//   scene (uploaded once, ps_scene):  fp64 SoA mean_x/y/z, scale_x/y/z, rot_w/x/y/z,
+//                                     opacity (88 B/splat) + SH as 12 float4 per splat
+//                                     sh4[i*12 + j] (the Splat3D coefficient order;
+//                                     192 B/splat at degree 3)
+//   frame (per render, ps_ctx):       depth keys/values for the depth sort, tight tile
+//                                     counts, fp64 mean2d / conic / culling root / rect
+//                                     (for duplicate-with-keys and the exact fp64 paths)
+//                                     and the fp32 blend record (48 B) per splat;
+//                                     tile pairs (key = tile id, value = splat index)
+//                                     in two ping-pong buffers; per-tile [start,end).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "polysplat_b200.h"
+
+namespace ps {
+
+constexpr int kShPlanes = 12; // 48 floats = 16 coefficients x 3 channels, as float4
+
+struct SceneDev {
+    int64_t n = 0;
+    double* mean[3] = {nullptr, nullptr, nullptr};
+    double* scale[3] = {nullptr, nullptr, nullptr};
+    double* rot[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* opacity = nullptr;
+    float4* sh4 = nullptr; // [n][kShPlanes]
+};
+
+// Device counters / status words (one struct per context, zeroed per render).
+struct DevCounters {
+    unsigned long long frustum;      // splats_frustum_culled
+    unsigned long long coarse;       // tile_pairs_coarse
+    unsigned long long tight;        // tile_pairs_after_tight_test (== P)
+    unsigned long long visible;      // V
+    unsigned long long evals;        // kernel_evaluations
+    unsigned long long blended;      // fragments_blended
+    unsigned long long replay_px;    // flagged pixels (replayed exactly in fp64)
+    unsigned long long exact_evals;  // ambiguous alpha decisions re-decided in fp64
+    unsigned int error;              // first ps_status raised on device (0 = none)
+    unsigned int error_index;        // splat index that raised it
+    unsigned int pairs_total;        // P as computed by the count scan
+    unsigned int pad;
+};
+
+// Per-splat frame arrays (indexed by original splat index).
+struct FrameDev {
+    unsigned long long* key = nullptr;  // depth bits (visible) or ~0 (culled)
+    unsigned long long* key_alt = nullptr;
+    uint32_t* val = nullptr;            // splat index (sort payload)
+    uint32_t* val_alt = nullptr;
+    uint32_t* tcount = nullptr;         // tight tile count (0 when not visible)
+    uint32_t* offset = nullptr;         // exclusive scan of tcount in depth order
+    double2* mean2d = nullptr;          // fp64 (mx, my)
+    double2* conic_ab = nullptr;        // fp64 (a, b)
+    double2* conic_cq = nullptr;        // fp64 (c, culling quadric root incl. slack)
+    ushort4* rect = nullptr;            // inclusive tile rect (x0, y0, x1, y1)
+    double* opacity_eff = nullptr;      // fp64 opacity_eff
+    float4* bl0 = nullptr;              // fp32 blend record: A, beta, gamma, q_hi
+    float4* bl1 = nullptr;              //   q_lo, o (or log2 o), eT, color r
+    float2* bl2 = nullptr;              //   color g, b
+    double* cov_aa = nullptr;           // [3n] only for ps_prepare (debug); may be null
+    // tile pairs (length capacity P)
+    uint32_t* pkey = nullptr;
+    uint32_t* pkey_alt = nullptr;
+    uint32_t* pval = nullptr;
+    uint32_t* pval_alt = nullptr;
+    uint2* ranges = nullptr;            // per tile [start, end)
+    uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
+    double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)
+};
+
+// Blend-kernel parameters derived on the host from ps_config.
+enum ThresholdMode : int {
+    kQuadricThreshold = 0, // alpha >= eps  <=>  q <= q*(o): skip test in quadric space
+    kAlphaThreshold = 1,   // non-monotone kernel: skip test on the fp32 alpha
+};
+
+struct KernelF32 {
+    int kind;
+    int order;
+    float c[4];
+    float first_root;
+};
+
+struct FrameParams {
+    ps_camera cam;
+    ps_config cfg;
+    int tiles_x, tiles_y;
+    int sh_floats4;         // float4 planes to read for cfg.sh_degree
+    int threshold_mode;     // ThresholdMode
+    KernelF32 kf;           // blend kernel in fp32
+    float eps_f, floor_f;
+};
+
+#define PS_CUDA_TRY(expr)                                                  \
+    do {                                                                   \
+        cudaError_t _e = (expr);                                           \
+        if (_e != cudaSuccess) return ::ps::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+    } while (0)
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+} // namespace ps

@@ -1,0 +1,780 @@
+// context.cu — host runtime behind the C ABI (include/polysplat_b200.h):
+// contexts (device, stream, events, device scratch sized for the largest
+// scene/frame seen), device-resident scenes, and the per-frame pipeline
+//   K1 preprocess -> K2 depth sort -> K3 scan + duplicate-with-keys ->
+//   K4 tile sort -> K5 ranges -> K6 blend -> K7 exact replay.
+// One host sync per frame (after the count scan, to size the pair buffers and
+// surface device-side errors), plus the final copy-out.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "polysplat_b200.h"
+
+namespace ps {
+
+thread_local std::string g_free_error;
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    g_free_error = buf;
+    return e == cudaErrorMemoryAllocation ? PS_OUT_OF_MEMORY : PS_CUDA_ERROR;
+}
+
+// host restatements compiled in hostmath.cpp (same exact_math.cuh source)
+int host_validate_config(const ps_config& c);
+int host_validate_camera(const ps_camera& c);
+int host_kernel_threshold_mode(const ps_kernel& k);
+
+} // namespace ps
+
+using namespace ps;
+
+struct ps_scene {
+    ps_ctx* ctx = nullptr;
+    SceneDev dev;
+    void* block = nullptr;
+    int64_t n = 0;
+};
+
+struct ps_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool timing = false;
+    cudaEvent_t ev[PS_STAGE_COUNT + 1] = {};
+    ps_stats stats{};
+
+    // frame scratch
+    int64_t n_cap = 0;
+    int64_t p_cap = 0;
+    int64_t pix_cap = 0;
+    int64_t tiles_cap = 0;
+    FrameDev f;
+    void* n_block = nullptr;
+    void* p_block = nullptr;
+    void* radix_scratch = nullptr;
+    size_t radix_scratch_size = 0;
+    void* scan_scratch = nullptr;
+    size_t scan_scratch_size = 0;
+    float* img_rgb = nullptr;
+    float* img_t = nullptr;
+    double* cov_dbg = nullptr;
+    int64_t cov_dbg_cap = 0;
+    double4* replay_vals = nullptr;
+    DevCounters* d_ctr = nullptr;
+    DevCounters* h_ctr = nullptr; // pinned
+    void* stage = nullptr;        // scene upload staging
+    size_t stage_bytes = 0;
+};
+
+namespace {
+
+int set_err(ps_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    g_free_error = msg;
+    return code;
+}
+
+int cuda_err(ps_ctx* c, cudaError_t e, const char* what) {
+    int code = cuda_fail(e, what, __FILE__, __LINE__);
+    if (c) c->err = g_free_error;
+    return code;
+}
+
+#define CTX_TRY(c, expr)                                  \
+    do {                                                  \
+        cudaError_t _e = (expr);                          \
+        if (_e != cudaSuccess) return cuda_err(c, _e, #expr); \
+    } while (0)
+
+const char* status_message(int st) {
+    switch (st) {
+        case PS_INVALID_ARGUMENT: return "invalid argument";
+        case PS_NON_ORTHONORMAL_ROTATION: return "camera rotation is not orthonormal";
+        case PS_DEGENERATE_COVARIANCE: return "dilated 2D covariance is singular";
+        case PS_NO_POSITIVE_ROOT: return "polynomial has no positive root";
+        case PS_EPSILON_ZERO_UNBOUNDED: return "exponential kernel has unbounded support at epsilon 0";
+        case PS_FULLY_CULLED: return "opacity below cutoff";
+        default: return "error";
+    }
+}
+
+template <typename T>
+T* carve(char*& p, int64_t count) {
+    T* r = reinterpret_cast<T*>(p);
+    size_t bytes = sizeof(T) * static_cast<size_t>(count);
+    bytes = (bytes + 255) & ~size_t(255);
+    p += bytes;
+    return r;
+}
+
+size_t frame_bytes(int64_t n) {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    size_t s = 0;
+    s += 2 * al(8 * n) + 2 * al(4 * n) + 2 * al(4 * n); // key, key_alt, val, val_alt, tcount, offset
+    s += 3 * al(16 * n);                                 // mean2d, conic_ab, conic_cq
+    s += al(8 * n) + al(8 * n);                          // rect, opacity_eff
+    s += 2 * al(16 * n) + al(8 * n);                     // bl0, bl1, bl2
+    return s;
+}
+
+int ensure_frame(ps_ctx* c, int64_t n) {
+    if (n <= c->n_cap) return PS_OK;
+    int64_t cap = std::max<int64_t>(n, 1024);
+    if (c->n_block) cudaFree(c->n_block);
+    c->n_block = nullptr;
+    c->n_cap = 0;
+    CTX_TRY(c, cudaMalloc(&c->n_block, frame_bytes(cap)));
+    char* p = static_cast<char*>(c->n_block);
+    c->f.key = carve<unsigned long long>(p, cap);
+    c->f.key_alt = carve<unsigned long long>(p, cap);
+    c->f.val = carve<uint32_t>(p, cap);
+    c->f.val_alt = carve<uint32_t>(p, cap);
+    c->f.tcount = carve<uint32_t>(p, cap);
+    c->f.offset = carve<uint32_t>(p, cap);
+    c->f.mean2d = carve<double2>(p, cap);
+    c->f.conic_ab = carve<double2>(p, cap);
+    c->f.conic_cq = carve<double2>(p, cap);
+    c->f.rect = carve<ushort4>(p, cap);
+    c->f.opacity_eff = carve<double>(p, cap);
+    c->f.bl0 = carve<float4>(p, cap);
+    c->f.bl1 = carve<float4>(p, cap);
+    c->f.bl2 = carve<float2>(p, cap);
+    size_t rs = radix_scratch_bytes(cap);
+    size_t ss = scan_scratch_bytes(cap);
+    if (rs > c->radix_scratch_size) {
+        if (c->radix_scratch) cudaFree(c->radix_scratch);
+        c->radix_scratch = nullptr;
+        CTX_TRY(c, cudaMalloc(&c->radix_scratch, rs));
+        c->radix_scratch_size = rs;
+    }
+    if (ss > c->scan_scratch_size) {
+        if (c->scan_scratch) cudaFree(c->scan_scratch);
+        c->scan_scratch = nullptr;
+        CTX_TRY(c, cudaMalloc(&c->scan_scratch, ss));
+        c->scan_scratch_size = ss;
+    }
+    c->n_cap = cap;
+    return PS_OK;
+}
+
+int ensure_pairs(ps_ctx* c, int64_t p) {
+    if (p <= c->p_cap) return PS_OK;
+    int64_t cap = std::max<int64_t>(p + p / 4, 1 << 16);
+    if (c->p_block) cudaFree(c->p_block);
+    c->p_block = nullptr;
+    c->p_cap = 0;
+    CTX_TRY(c, cudaMalloc(&c->p_block, 4 * ((sizeof(uint32_t) * cap + 255) & ~size_t(255))));
+    char* q = static_cast<char*>(c->p_block);
+    c->f.pkey = carve<uint32_t>(q, cap);
+    c->f.pkey_alt = carve<uint32_t>(q, cap);
+    c->f.pval = carve<uint32_t>(q, cap);
+    c->f.pval_alt = carve<uint32_t>(q, cap);
+    size_t rs = radix_scratch_bytes(cap);
+    if (rs > c->radix_scratch_size) {
+        if (c->radix_scratch) cudaFree(c->radix_scratch);
+        c->radix_scratch = nullptr;
+        CTX_TRY(c, cudaMalloc(&c->radix_scratch, rs));
+        c->radix_scratch_size = rs;
+    }
+    c->p_cap = cap;
+    return PS_OK;
+}
+
+int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
+    if (pix > c->pix_cap) {
+        if (c->img_rgb) cudaFree(c->img_rgb);
+        if (c->img_t) cudaFree(c->img_t);
+        if (c->f.flags) cudaFree(c->f.flags);
+        if (c->replay_vals) cudaFree(c->replay_vals);
+        c->img_rgb = nullptr; c->img_t = nullptr; c->f.flags = nullptr; c->replay_vals = nullptr;
+        c->pix_cap = 0;
+        CTX_TRY(c, cudaMalloc(&c->img_rgb, sizeof(float) * 3 * pix));
+        CTX_TRY(c, cudaMalloc(&c->img_t, sizeof(float) * pix));
+        CTX_TRY(c, cudaMalloc(&c->f.flags, sizeof(uint32_t) * pix));
+        CTX_TRY(c, cudaMalloc(&c->replay_vals, sizeof(double4) * pix));
+        c->pix_cap = pix;
+    }
+    if (n_tiles > c->tiles_cap) {
+        if (c->f.ranges) cudaFree(c->f.ranges);
+        c->f.ranges = nullptr;
+        c->tiles_cap = 0;
+        CTX_TRY(c, cudaMalloc(&c->f.ranges, sizeof(uint2) * n_tiles));
+        c->tiles_cap = n_tiles;
+    }
+    return PS_OK;
+}
+
+int bits_for(int64_t n_tiles) {
+    int b = 0;
+    while ((int64_t(1) << b) < n_tiles) ++b;
+    return std::max(b, 1);
+}
+
+enum class Mode { Render, CountPairs, Prepare, TileLists };
+
+struct FrameRequest {
+    Mode mode = Mode::Render;
+    float* d_rgb = nullptr; // device outputs (Render)
+    float* d_t = nullptr;
+    bool count_work = false;
+    bool want_replay_vals = false;
+};
+
+struct FrameResult {
+    int64_t visible = 0;
+    int64_t pairs = 0;
+    bool pairs_in_alt = false;
+    bool order_in_alt = false;
+    DevCounters ctr{};
+};
+
+void record(ps_ctx* c, int stage) {
+    if (c->timing) cudaEventRecord(c->ev[stage], c->stream);
+}
+
+int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_config& cfg_in,
+              const FrameRequest& req, FrameResult& res) {
+    int st = host_validate_config(cfg_in);
+    if (st != PS_OK) return set_err(c, st, "RasterConfig::validate: invalid configuration");
+    st = host_validate_camera(cam);
+    if (st != PS_OK)
+        return set_err(c, st, st == PS_NON_ORTHONORMAL_ROTATION ? "camera rotation is not orthonormal"
+                                                                 : "Camera::validate: invalid camera");
+    ps_config cfg = cfg_in;
+    if (cfg.sh_degree > 3) cfg.sh_degree = 3;
+    if (cfg.sh_degree < 0) cfg.sh_degree = -1;
+    if ((req.mode == Mode::Render) && cfg.tile_size > 32)
+        return set_err(c, PS_INVALID_ARGUMENT, "device blend supports tile_size <= 32");
+    if (cfg.kernel.kind != PS_KERNEL_EXPONENTIAL && (cfg.kernel.order < 1 || cfg.kernel.order > 3))
+        return set_err(c, PS_INVALID_ARGUMENT, "kernel order must be in {1,2,3}");
+    if (cfg.has_culling_kernel && cfg.culling_kernel.kind != PS_KERNEL_EXPONENTIAL &&
+        (cfg.culling_kernel.order < 1 || cfg.culling_kernel.order > 3))
+        return set_err(c, PS_INVALID_ARGUMENT, "culling kernel order must be in {1,2,3}");
+
+    const int64_t n = s->n;
+    FrameParams P;
+    std::memset(&P, 0, sizeof P);
+    P.cam = cam;
+    P.cfg = cfg;
+    P.tiles_x = (cam.width + cfg.tile_size - 1) / cfg.tile_size;
+    P.tiles_y = (cam.height + cfg.tile_size - 1) / cfg.tile_size;
+    const int sh_floats = cfg.sh_degree < 0 ? 0 : 3 * (cfg.sh_degree + 1) * (cfg.sh_degree + 1);
+    P.sh_floats4 = (sh_floats + 3) / 4;
+    P.threshold_mode = host_kernel_threshold_mode(cfg.kernel);
+    P.kf.kind = cfg.kernel.kind;
+    P.kf.order = cfg.kernel.order;
+    for (int j = 0; j < 4; ++j) P.kf.c[j] = static_cast<float>(cfg.kernel.coeffs[j]);
+    P.kf.first_root = static_cast<float>(cfg.kernel.first_root);
+    P.eps_f = static_cast<float>(cfg.epsilon);
+    P.floor_f = static_cast<float>(cfg.transmittance_floor);
+    const int n_tiles = P.tiles_x * P.tiles_y;
+    const int64_t pix = static_cast<int64_t>(cam.width) * cam.height;
+
+    CTX_TRY(c, cudaSetDevice(c->device));
+    if ((st = ensure_frame(c, n)) != PS_OK) return st;
+    if ((st = ensure_image(c, pix, n_tiles)) != PS_OK) return st;
+    FrameDev f = c->f;
+    f.cov_aa = nullptr;
+    f.replay_vals = req.want_replay_vals ? c->replay_vals : nullptr;
+    if (req.mode == Mode::Prepare) {
+        if (n * 3 > c->cov_dbg_cap) {
+            if (c->cov_dbg) cudaFree(c->cov_dbg);
+            c->cov_dbg = nullptr;
+            c->cov_dbg_cap = 0;
+            CTX_TRY(c, cudaMalloc(&c->cov_dbg, sizeof(double) * std::max<int64_t>(3 * n, 3)));
+            c->cov_dbg_cap = 3 * n;
+        }
+        f.cov_aa = c->cov_dbg;
+        P.cfg.clamp_before_blend = 0; // prepared colours are unclamped (projection.cpp:93-116)
+    }
+
+    int launches = 0;
+    cudaStream_t strm = c->stream;
+    CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
+    record(c, 0);
+    launch_preprocess(s->dev, P, f, c->d_ctr, strm);
+    launches += n > 0;
+    record(c, 1);
+    // K2: stable radix sort of the fp64 depth bits (positive doubles order as
+    // their bit patterns); culled splats carry ~0 and sort last.
+    bool oalt = radix_sort_u64(f.key, f.key_alt, f.val, f.val_alt, nullptr, n, 0, 64, c->radix_scratch,
+                               strm, &launches);
+    const uint32_t* order = oalt ? f.val_alt : f.val;
+    record(c, 2);
+    // K3a: exclusive scan of tight counts in depth order
+    scan_gathered_counts(f.tcount, order, f.offset, n, &c->d_ctr->pairs_total, c->scan_scratch, strm,
+                         &launches);
+    CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
+    CTX_TRY(c, cudaStreamSynchronize(strm));
+    CTX_TRY(c, cudaGetLastError());
+    res.ctr = *c->h_ctr;
+    res.visible = static_cast<int64_t>(res.ctr.visible);
+    res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
+    res.order_in_alt = oalt;
+    if (res.ctr.error) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
+                      res.ctr.error_index);
+        return set_err(c, static_cast<int>(res.ctr.error), buf);
+    }
+    if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
+        return set_err(c, PS_ERROR, "internal: pair scan disagrees with tight count");
+    if (req.mode == Mode::CountPairs || req.mode == Mode::Prepare) {
+        c->stats.visible = res.visible;
+        c->stats.pairs = res.pairs;
+        c->stats.kernel_launches = launches;
+        return PS_OK;
+    }
+
+    if ((st = ensure_pairs(c, res.pairs)) != PS_OK) return st;
+    f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
+    // K3b: duplicate-with-keys in depth order
+    launch_duplicate(f, P, order, n, strm);
+    launches += n > 0;
+    record(c, 3);
+    // K4: stable sort of pairs by tile id (depth order is preserved within a tile)
+    bool palt = radix_sort_u32(f.pkey, f.pkey_alt, f.pval, f.pval_alt, nullptr, res.pairs, 0,
+                               bits_for(n_tiles), c->radix_scratch, strm, &launches);
+    res.pairs_in_alt = palt;
+    const uint32_t* skeys = palt ? f.pkey_alt : f.pkey;
+    const uint32_t* svals = palt ? f.pval_alt : f.pval;
+    record(c, 4);
+    // K5: tile ranges
+    launch_ranges(skeys, nullptr, res.pairs, f.ranges, n_tiles, strm, &launches);
+    record(c, 5);
+    if (req.mode == Mode::TileLists) {
+        CTX_TRY(c, cudaStreamSynchronize(strm));
+        CTX_TRY(c, cudaGetLastError());
+        c->stats.visible = res.visible;
+        c->stats.pairs = res.pairs;
+        c->stats.kernel_launches = launches;
+        return PS_OK;
+    }
+    // K6: blend
+    BlendOut out{req.d_rgb, req.d_t};
+    launches += launch_blend(f, P, svals, c->d_ctr, out, req.count_work, strm);
+    record(c, 6);
+    // K7: exact replay of flagged pixels (grid-stride over the device-side count)
+    FrameDev fr = f;
+    fr.pval = const_cast<uint32_t*>(svals);
+    launch_replay(fr, P, c->d_ctr, req.d_rgb, req.d_t, req.count_work, c->sm_count, strm);
+    launches += 1;
+    record(c, 7);
+    CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
+    CTX_TRY(c, cudaStreamSynchronize(strm));
+    CTX_TRY(c, cudaGetLastError());
+    res.ctr = *c->h_ctr;
+    c->stats.visible = res.visible;
+    c->stats.pairs = res.pairs;
+    c->stats.replay_pixels = res.ctr.replay_px;
+    c->stats.exact_alpha_evals = res.ctr.exact_evals;
+    c->stats.kernel_launches = launches;
+    if (c->timing) {
+        const int map[PS_STAGE_COUNT][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}};
+        for (int k = 0; k < PS_STAGE_COUNT; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev[map[k][0]], c->ev[map[k][1]]);
+            c->stats.stage_ms[k] = ms;
+        }
+    }
+    return PS_OK;
+}
+
+void fill_counters(ps_counters* out, const ps_scene* s, const FrameResult& r, bool with_work) {
+    if (!out) return;
+    out->splats_submitted = static_cast<uint64_t>(s->n);
+    out->splats_frustum_culled = r.ctr.frustum;
+    out->tile_pairs_coarse = r.ctr.coarse;
+    out->tile_pairs_after_tight_test = r.ctr.tight;
+    out->kernel_evaluations = with_work ? r.ctr.evals : 0;
+    out->fragments_blended = with_work ? r.ctr.blended : 0;
+}
+
+int render_one(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg, float* out_rgb,
+               float* out_t, int memspace, ps_counters* counters, bool want_replay_vals,
+               FrameResult* res_out) {
+    if (!c || !s || !cam || !cfg) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    if (s->ctx != c) return set_err(c, PS_INVALID_ARGUMENT, "scene belongs to another context");
+    const int64_t pix = static_cast<int64_t>(cam->width) * cam->height;
+    int st = PS_OK;
+    if (pix > 0 && (st = ensure_image(c, pix, 1)) != PS_OK) return st;
+    FrameRequest req;
+    req.mode = Mode::Render;
+    const bool dev_out = memspace == PS_MEM_DEVICE;
+    req.d_rgb = dev_out && out_rgb ? out_rgb : c->img_rgb;
+    req.d_t = dev_out && out_t ? out_t : c->img_t;
+    req.count_work = counters != nullptr;
+    req.want_replay_vals = want_replay_vals;
+    FrameResult r;
+    st = run_frame(c, s, *cam, *cfg, req, r);
+    if (st != PS_OK) return st;
+    if (!dev_out) {
+        if (out_rgb)
+            CTX_TRY(c, cudaMemcpyAsync(out_rgb, req.d_rgb, sizeof(float) * 3 * pix, cudaMemcpyDeviceToHost, c->stream));
+        if (out_t)
+            CTX_TRY(c, cudaMemcpyAsync(out_t, req.d_t, sizeof(float) * pix, cudaMemcpyDeviceToHost, c->stream));
+        CTX_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    fill_counters(counters, s, r, true);
+    if (res_out) *res_out = r;
+    return PS_OK;
+}
+
+int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales, const double* rots,
+               const double* opac, const float* sh, int memspace) {
+    const int64_t n = s->n;
+    if (n == 0) return PS_OK;
+    const cudaMemcpyKind kind = memspace == PS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // means/scales/rotations arrive interleaved per splat (n x 3 / n x 4): copy
+    // them raw into a staging buffer (three large DMAs; full PCIe/C2C rate when
+    // the host buffers are pinned) and de-interleave into planes on the device.
+    const size_t stage_bytes = sizeof(double) * 10 * static_cast<size_t>(n);
+    if (stage_bytes > c->stage_bytes) {
+        if (c->stage) cudaFree(c->stage);
+        c->stage = nullptr;
+        c->stage_bytes = 0;
+        CTX_TRY(c, cudaMalloc(&c->stage, stage_bytes));
+        c->stage_bytes = stage_bytes;
+    }
+    double* st = static_cast<double*>(c->stage);
+    CTX_TRY(c, cudaMemcpyAsync(st, means, sizeof(double) * 3 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(s->dev.opacity, opac, sizeof(double) * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(s->dev.sh4, sh, sizeof(float) * 48 * n, kind, c->stream));
+    launch_deinterleave(st, n, s->dev, c->stream);
+    CTX_TRY(c, cudaStreamSynchronize(c->stream));
+    CTX_TRY(c, cudaGetLastError());
+    return PS_OK;
+}
+
+int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
+    auto* s = new ps_scene();
+    s->ctx = c;
+    s->n = n;
+    s->dev.n = n;
+    const int64_t cap = std::max<int64_t>(n, 1);
+    const size_t plane = (sizeof(double) * cap + 255) & ~size_t(255);
+    const size_t shb = (sizeof(float) * 48 * cap + 255) & ~size_t(255);
+    cudaError_t e = cudaMalloc(&s->block, 11 * plane + shb);
+    if (e != cudaSuccess) {
+        delete s;
+        return cuda_err(c, e, "cudaMalloc(scene)");
+    }
+    char* p = static_cast<char*>(s->block);
+    for (int k = 0; k < 3; ++k) { s->dev.mean[k] = reinterpret_cast<double*>(p); p += plane; }
+    for (int k = 0; k < 3; ++k) { s->dev.scale[k] = reinterpret_cast<double*>(p); p += plane; }
+    for (int k = 0; k < 4; ++k) { s->dev.rot[k] = reinterpret_cast<double*>(p); p += plane; }
+    s->dev.opacity = reinterpret_cast<double*>(p); p += plane;
+    s->dev.sh4 = reinterpret_cast<float4*>(p);
+    *out = s;
+    return PS_OK;
+}
+
+} // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* ps_version(void) { return "polysplat-b200 0.1 (sm_100a)"; }
+int ps_abi_version(void) { return PS_ABI_VERSION; }
+
+int ps_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int ps_ctx_create(int device, ps_ctx** out) {
+    if (!out) return set_err(nullptr, PS_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_err(nullptr, PS_CUDA_ERROR, "no CUDA device available: the B200 path has no CPU fallback");
+    }
+    if (device < 0 || device >= n) return set_err(nullptr, PS_INVALID_ARGUMENT, "device index out of range");
+    auto* c = new ps_ctx();
+    c->device = device;
+    auto fail = [&](cudaError_t err, const char* what) {
+        int code = cuda_err(c, err, what);
+        ps_ctx_destroy(c);
+        return code;
+    };
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e, "cudaSetDevice");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return fail(e, "cudaGetDeviceProperties");
+    if (prop.major < 10) {
+        ps_ctx_destroy(c);
+        return set_err(nullptr, PS_CUDA_ERROR, "device is not sm_100-class (Blackwell) — this build targets sm_100a");
+    }
+    c->sm_count = prop.multiProcessorCount;
+    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "stream");
+    for (auto& ev : c->ev)
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(e, "event");
+    if ((e = cudaMalloc(&c->d_ctr, sizeof(DevCounters))) != cudaSuccess) return fail(e, "counters");
+    if ((e = cudaMallocHost(&c->h_ctr, sizeof(DevCounters))) != cudaSuccess) return fail(e, "pinned counters");
+    *out = c;
+    return PS_OK;
+}
+
+void ps_ctx_destroy(ps_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& ev : c->ev)
+        if (ev) cudaEventDestroy(ev);
+    void* bufs[] = {c->n_block, c->p_block, c->radix_scratch, c->scan_scratch, c->img_rgb, c->img_t,
+                    c->f.flags, c->f.ranges, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* ps_last_error(const ps_ctx* c) { return c ? c->err.c_str() : g_free_error.c_str(); }
+
+int ps_ctx_set_timing(ps_ctx* c, int enabled) {
+    if (!c) return PS_INVALID_ARGUMENT;
+    c->timing = enabled != 0;
+    return PS_OK;
+}
+
+int ps_last_stats(const ps_ctx* c, ps_stats* out) {
+    if (!c || !out) return PS_INVALID_ARGUMENT;
+    *out = c->stats;
+    return PS_OK;
+}
+
+int ps_ctx_synchronize(ps_ctx* c) {
+    if (!c) return PS_INVALID_ARGUMENT;
+    CTX_TRY(c, cudaStreamSynchronize(c->stream));
+    return PS_OK;
+}
+
+void* ps_ctx_stream(ps_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int ps_measure_fp32_peak(ps_ctx* c, double* tflops) {
+    if (!c || !tflops) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    *tflops = measure_fp32_tflops(c->sm_count, c->stream);
+    CTX_TRY(c, cudaGetLastError());
+    return PS_OK;
+}
+
+int ps_scene_create_soa(ps_ctx* c, const double* means, const double* scales, const double* rotations,
+                        const double* opacities, const float* sh, int64_t n, int memspace, ps_scene** out) {
+    if (!c || !out || n < 0) return set_err(c, PS_INVALID_ARGUMENT, "bad scene arguments");
+    if (n > 0 && (!means || !scales || !rotations || !opacities || !sh))
+        return set_err(c, PS_INVALID_ARGUMENT, "null scene array");
+    if (n > 0xFFFFFFFFll) return set_err(c, PS_INVALID_ARGUMENT, "scene too large (> 2^32 splats)");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    ps_scene* s = nullptr;
+    int st = alloc_scene(c, n, &s);
+    if (st != PS_OK) return st;
+    st = upload_soa(c, s, means, scales, rotations, opacities, sh, memspace);
+    if (st != PS_OK) {
+        ps_scene_destroy(s);
+        return st;
+    }
+    *out = s;
+    return PS_OK;
+}
+
+int ps_scene_update_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales,
+                        const double* rotations, const double* opacities, const float* sh, int memspace) {
+    if (!c || !s || s->ctx != c) return set_err(c, PS_INVALID_ARGUMENT, "bad scene");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    return upload_soa(c, s, means, scales, rotations, opacities, sh, memspace);
+}
+
+int ps_scene_create_aos(ps_ctx* c, const double* splats, int64_t n, ps_scene** out) {
+    if (!c || !out || n < 0 || (n > 0 && !splats)) return set_err(c, PS_INVALID_ARGUMENT, "bad scene arguments");
+    const int64_t cap = std::max<int64_t>(n, 1);
+    std::vector<double> means(3 * cap), scales(3 * cap), rots(4 * cap), opac(cap);
+    std::vector<float> sh(48 * cap);
+    for (int64_t i = 0; i < n; ++i) {
+        const double* sp = splats + i * PS_SPLAT3D_DOUBLES;
+        for (int k = 0; k < 3; ++k) means[3 * i + k] = sp[k];
+        for (int k = 0; k < 3; ++k) scales[3 * i + k] = sp[3 + k];
+        for (int k = 0; k < 4; ++k) rots[4 * i + k] = sp[6 + k];
+        opac[i] = sp[10];
+        for (int k = 0; k < 48; ++k) sh[48 * i + k] = static_cast<float>(sp[11 + k]);
+    }
+    return ps_scene_create_soa(c, means.data(), scales.data(), rots.data(), opac.data(), sh.data(), n,
+                               PS_MEM_HOST, out);
+}
+
+int64_t ps_scene_size(const ps_scene* s) { return s ? s->n : -1; }
+
+void ps_scene_destroy(ps_scene* s) {
+    if (!s) return;
+    if (s->block) {
+        cudaSetDevice(s->ctx->device);
+        cudaStreamSynchronize(s->ctx->stream);
+        cudaFree(s->block);
+    }
+    delete s;
+}
+
+int ps_render(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg, float* out_rgb,
+              float* out_t, int memspace, ps_counters* counters) {
+    return render_one(c, s, cam, cfg, out_rgb, out_t, memspace, counters, false, nullptr);
+}
+
+int ps_render_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, int n_views, const ps_config* cfg,
+                    float* out_rgb, float* out_t, int memspace, ps_counters* counters) {
+    if (!c || !s || !cams || n_views < 0) return set_err(c, PS_INVALID_ARGUMENT, "bad arguments");
+    for (int v = 0; v < n_views; ++v) {
+        if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+            return set_err(c, PS_INVALID_ARGUMENT, "all views must share width/height");
+    }
+    const int64_t pix = n_views ? static_cast<int64_t>(cams[0].width) * cams[0].height : 0;
+    for (int v = 0; v < n_views; ++v) {
+        int st = render_one(c, s, &cams[v], cfg, out_rgb ? out_rgb + 3 * pix * v : nullptr,
+                            out_t ? out_t + pix * v : nullptr, memspace, counters ? counters + v : nullptr,
+                            false, nullptr);
+        if (st != PS_OK) return st;
+    }
+    return PS_OK;
+}
+
+int ps_render_splats(ps_ctx* c, const double* splats, int64_t n, const ps_camera* cam, const ps_config* cfg,
+                     double* out_rgb, double* out_t, ps_counters* counters) {
+    if (!c || !cam || !cfg) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    int st = host_validate_config(*cfg);
+    if (st != PS_OK) return set_err(c, st, "RasterConfig::validate: invalid configuration");
+    st = host_validate_camera(*cam);
+    if (st != PS_OK) return set_err(c, st, "Camera::validate: invalid camera");
+    ps_scene* s = nullptr;
+    if ((st = ps_scene_create_aos(c, splats, n, &s)) != PS_OK) return st;
+    const int64_t pix = static_cast<int64_t>(cam->width) * cam->height;
+    std::vector<float> rgb(3 * pix), tr(pix);
+    FrameResult r;
+    st = render_one(c, s, cam, cfg, rgb.data(), tr.data(), PS_MEM_HOST, counters, true, &r);
+    if (st == PS_OK) {
+        for (int64_t k = 0; k < 3 * pix; ++k) if (out_rgb) out_rgb[k] = rgb[k];
+        for (int64_t k = 0; k < pix; ++k) if (out_t) out_t[k] = tr[k];
+        const unsigned long long nf = r.ctr.replay_px;
+        if (nf) {
+            std::vector<uint32_t> ids(nf);
+            std::vector<double4> vals(nf);
+            cudaMemcpy(ids.data(), c->f.flags, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost);
+            cudaMemcpy(vals.data(), c->replay_vals, sizeof(double4) * nf, cudaMemcpyDeviceToHost);
+            for (unsigned long long k = 0; k < nf; ++k) {
+                const uint32_t p = ids[k];
+                if (out_rgb) { out_rgb[3 * p] = vals[k].x; out_rgb[3 * p + 1] = vals[k].y; out_rgb[3 * p + 2] = vals[k].z; }
+                if (out_t) out_t[p] = vals[k].w;
+            }
+        }
+    }
+    ps_scene_destroy(s);
+    return st;
+}
+
+int ps_count_pairs(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg,
+                   ps_counters* counters) {
+    if (!c || !s || !cam || !cfg) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    FrameRequest req;
+    req.mode = Mode::CountPairs;
+    FrameResult r;
+    int st = run_frame(c, s, *cam, *cfg, req, r);
+    if (st != PS_OK) return st;
+    fill_counters(counters, s, r, false);
+    return PS_OK;
+}
+
+int ps_prepare(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg, int64_t capacity,
+               const ps_prepared* out, int64_t* n_out, ps_counters* counters) {
+    if (!c || !s || !cam || !cfg || !n_out) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    FrameRequest req;
+    req.mode = Mode::Prepare;
+    FrameResult r;
+    int st = run_frame(c, s, *cam, *cfg, req, r);
+    if (st != PS_OK) return st;
+    fill_counters(counters, s, r, false);
+    const int64_t v = r.visible;
+    *n_out = v;
+    if (!out || v == 0) return PS_OK; // size query
+    if (v > capacity) return set_err(c, PS_INVALID_ARGUMENT, "capacity too small");
+    const FrameDev& f = c->f;
+    const uint32_t* order = r.order_in_alt ? f.val_alt : f.val;
+    const unsigned long long* keys = r.order_in_alt ? f.key_alt : f.key;
+    std::vector<uint32_t> idx(v);
+    std::vector<unsigned long long> kk(v);
+    CTX_TRY(c, cudaMemcpy(idx.data(), order, sizeof(uint32_t) * v, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(kk.data(), keys, sizeof(unsigned long long) * v, cudaMemcpyDeviceToHost));
+    const int64_t n = s->n;
+    std::vector<double2> m(n), ab(n), cq(n);
+    std::vector<double> o(n), cov(3 * n);
+    std::vector<float4> b1(n);
+    std::vector<float2> b2(n);
+    CTX_TRY(c, cudaMemcpy(m.data(), f.mean2d, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(ab.data(), f.conic_ab, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(cq.data(), f.conic_cq, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(o.data(), f.opacity_eff, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(cov.data(), c->cov_dbg, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(b1.data(), f.bl1, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+    CTX_TRY(c, cudaMemcpy(b2.data(), f.bl2, sizeof(float2) * n, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < v; ++k) {
+        const uint32_t i = idx[k];
+        if (out->index) out->index[k] = i;
+        if (out->depth) { double d; std::memcpy(&d, &kk[k], 8); out->depth[k] = d; }
+        if (out->mean2d) { out->mean2d[2 * k] = m[i].x; out->mean2d[2 * k + 1] = m[i].y; }
+        if (out->conic) { out->conic[3 * k] = ab[i].x; out->conic[3 * k + 1] = ab[i].y; out->conic[3 * k + 2] = cq[i].x; }
+        if (out->cov_aa) for (int j = 0; j < 3; ++j) out->cov_aa[3 * k + j] = cov[3 * i + j];
+        if (out->opacity_eff) out->opacity_eff[k] = o[i];
+        if (out->color) { out->color[3 * k] = b1[i].w; out->color[3 * k + 1] = b2[i].x; out->color[3 * k + 2] = b2[i].y; }
+        if (out->quadric_root) out->quadric_root[k] = cq[i].y;
+        if (out->radius_sigma) out->radius_sigma[k] = std::sqrt(cq[i].y);
+    }
+    return PS_OK;
+}
+
+int ps_tile_lists(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg, int64_t capacity,
+                  uint32_t* tile_offsets, uint32_t* splat_index, int64_t* n_pairs, ps_counters* counters) {
+    if (!c || !s || !cam || !cfg || !n_pairs) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    FrameRequest req;
+    req.mode = Mode::TileLists;
+    FrameResult r;
+    int st = run_frame(c, s, *cam, *cfg, req, r);
+    if (st != PS_OK) return st;
+    fill_counters(counters, s, r, false);
+    *n_pairs = r.pairs;
+    if (!tile_offsets && !splat_index) return PS_OK; // size query
+    if (r.pairs > capacity) return set_err(c, PS_INVALID_ARGUMENT, "capacity too small");
+    const int ts = cfg->tile_size;
+    const int n_tiles = ((cam->width + ts - 1) / ts) * ((cam->height + ts - 1) / ts);
+    std::vector<uint2> rng(n_tiles);
+    CTX_TRY(c, cudaMemcpy(rng.data(), c->f.ranges, sizeof(uint2) * n_tiles, cudaMemcpyDeviceToHost));
+    if (tile_offsets) {
+        // tiles without pairs carry [0,0); rebuild a monotone CSR
+        uint32_t run = 0;
+        for (int t = 0; t < n_tiles; ++t) {
+            if (rng[t].y > rng[t].x) { tile_offsets[t] = rng[t].x; run = rng[t].y; }
+            else tile_offsets[t] = run;
+        }
+        tile_offsets[n_tiles] = static_cast<uint32_t>(r.pairs);
+    }
+    if (splat_index && r.pairs)
+        CTX_TRY(c, cudaMemcpy(splat_index, r.pairs_in_alt ? c->f.pval_alt : c->f.pval,
+                              sizeof(uint32_t) * r.pairs, cudaMemcpyDeviceToHost));
+    return PS_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,54 @@
+// kernels.h — host-side launchers of the rasterizer stages (one per .cu TU).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ps {
+
+// exact_kernels.cu (-fmad=false)
+void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
+                       cudaStream_t st);
+void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
+                      cudaStream_t st);
+void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
+                   float* out_t, bool count_work, int sm_count, cudaStream_t st);
+
+// sort.cu — stable LSD radix sort (8-bit digits) of (key, uint32 value) pairs.
+// The item count is read from device memory (*d_n), capped at n_cap; the grid
+// is sized for n_cap. Sorts bits [begin_bit, end_bit). Ping-pongs between
+// (keys, vals) and (keys_alt, vals_alt); returns true when the result ends in
+// the *_alt buffers. scratch must hold radix_scratch_bytes(n_cap) bytes.
+size_t radix_scratch_bytes(int64_t n_cap);
+bool radix_sort_u64(unsigned long long* keys, unsigned long long* keys_alt, uint32_t* vals,
+                    uint32_t* vals_alt, const uint32_t* d_n, int64_t n_cap, int begin_bit, int end_bit,
+                    void* scratch, cudaStream_t st, int* launches);
+bool radix_sort_u32(uint32_t* keys, uint32_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
+                    const uint32_t* d_n, int64_t n_cap, int begin_bit, int end_bit, void* scratch,
+                    cudaStream_t st, int* launches);
+
+// Exclusive scan of tcount[order[r]] over r < n into offset[r]; the total goes
+// to *d_total. scratch: scan_scratch_bytes(n).
+size_t scan_scratch_bytes(int64_t n);
+void scan_gathered_counts(const uint32_t* tcount, const uint32_t* order, uint32_t* offset, int64_t n,
+                          uint32_t* d_total, void* scratch, cudaStream_t st, int* launches);
+
+// per-tile [start, end) over sorted tile keys (K5)
+void launch_ranges(const uint32_t* keys, const uint32_t* d_n, int64_t n_cap, uint2* ranges,
+                   int n_tiles, cudaStream_t st, int* launches);
+
+// blend.cu (K6)
+struct BlendOut {
+    float* rgb;
+    float* t;
+};
+int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, DevCounters* ctr,
+                 BlendOut out, bool count_work, cudaStream_t st);
+
+// utils.cu
+void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st);
+double measure_fp32_tflops(int sm_count, cudaStream_t st);
+
+} // namespace ps
