@@ -74,7 +74,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -91,7 +91,7 @@ class ClockSampler:
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
@@ -314,10 +314,8 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
     sh_bytes = 12 * (deg + 1) ** 2
     work = {  # SURVEY §8(d) algorithmic work per stage
         "preprocess": ("hbm", n * (88 + sh_bytes) + v * 64),
-        "depth_sort": ("hbm", v * 12 * 2),
         "duplicate": ("hbm", p * 12),
         "tile_sort": ("hbm", p * 12 * 2),
-        "ranges": ("hbm", p * 8),
         "blend": ("fp32", OPS_PER_EVAL.get(kname, 8) * E + OPS_PER_BLEND * B),
     }
     out = {}
@@ -372,8 +370,8 @@ def cpu_baseline(workload: str) -> dict:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="c2")
     ap.add_argument("--no-compare", action="store_true")

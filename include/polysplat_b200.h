@@ -121,13 +121,13 @@ typedef struct ps_counters {
  * reference; reported by the bench). Stage times are CUDA-event milliseconds
  * on the context stream, filled only when timing is enabled. */
 enum {
-    PS_STAGE_PREPROCESS = 0,
-    PS_STAGE_DEPTH_SORT = 1,
-    PS_STAGE_DUPLICATE = 2,
-    PS_STAGE_TILE_SORT = 3,
-    PS_STAGE_RANGES = 4,
-    PS_STAGE_BLEND = 5,
-    PS_STAGE_REPLAY = 6,
+    PS_STAGE_PREPROCESS = 0, /* K1: projection, bounds, tight tile counts, blend records */
+    PS_STAGE_TILE_SCAN = 1,  /* K2: per-tile ranges / bucket cursors */
+    PS_STAGE_HOST_SYNC = 2,  /* the one mid-frame host round trip (sizes pair buffers) */
+    PS_STAGE_DUPLICATE = 3,  /* K3: splat indices into per-tile buckets */
+    PS_STAGE_TILE_SORT = 4,  /* K4: exact (depth, index) order per bucket */
+    PS_STAGE_BLEND = 5,      /* K6: fp32 blend with exact decisions */
+    PS_STAGE_REPLAY = 6,     /* K7: fp64 replay of flagged pixels */
     PS_STAGE_COUNT = 7
 };
 typedef struct ps_stats {

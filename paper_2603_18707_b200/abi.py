@@ -40,7 +40,7 @@ PS_CULL_OPACITY_AWARE = 2
 PS_MEM_HOST = 0
 PS_MEM_DEVICE = 1
 
-STAGES = ("preprocess", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "replay")
+STAGES = ("preprocess", "tile_scan", "host_sync", "duplicate", "tile_sort", "blend", "replay")
 
 
 class ps_kernel(C.Structure):

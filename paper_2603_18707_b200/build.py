@@ -42,6 +42,7 @@ SOURCES = [
     ("exact_kernels.cu", ["-fmad=false"]),
     ("blend.cu", []),
     ("sort.cu", []),
+    ("binning.cu", []),
     ("utils.cu", []),
     ("context.cu", []),
     ("hostmath.cpp", []),

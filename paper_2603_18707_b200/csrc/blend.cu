@@ -216,6 +216,236 @@ __global__ void k_blend(const BlendArgs A) {
     }
 }
 
+// ---------------------------------------------------------------- 16x16 fast path
+// tile_size == 16: 128 threads, two pixels per thread in the same row (x and
+// x+8), so the per-row terms (dy, the row-shifted centre, gamma dy^2) are
+// shared. Batches of 128 records live in static shared memory (immediate
+// offsets in the inner loop) and the next batch is prefetched into registers
+// while the current one is blended. A finished pixel gets x = NaN, which makes
+// its quadric NaN and the skip test `!(q <= q_hi)` true: no per-pixel branch.
+constexpr int kB16 = 128;
+constexpr float kNaNf = __builtin_nanf("");
+
+struct Px {
+    float x;      // tile-local pixel-centre x (NaN once the pixel is finished)
+    float T, r, g, b, eT;
+    uint32_t term, nbl;
+    bool flagged;
+};
+
+// Shared-memory record of one staged splat (tile-local, fp32):
+//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, K0}  c = {eT, r, g, b}
+//   d = {K1, K2, K3, splat index bits}   box = {x_lo, x_hi, y_lo, y_hi}
+// K_j = o c_j folds the opacity into the polynomial (K0 = log2 o for exp);
+// box is the axis-aligned extent of {q <= q_hi} (+ margin) used for warp culling.
+template <int KIND, int ORDER, int MODE, bool COUNT>
+__device__ __forceinline__ void blend_px(Px& p, float q, const float4& sb, const float4& sc, const float4& sd,
+                                         const BlendArgs& A, int gx, int gy, int jpos, uint32_t& nexact) {
+    float alpha;
+    if (MODE == kQuadricThreshold) {
+        if (q >= sb.z) { // inside the certified fp32 error band: decide with fp64
+            ++nexact;
+            if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, __float_as_uint(sd.w), gx, gy))
+                return;
+        }
+        // Accepted fragments have q < q* + Gq < first_root, where the ReLU /
+        // piecewise cut-offs are inactive: alpha = min(.999, sum K_j q^j).
+        if (KIND == 0) {
+            alpha = fminf(0.999f, ex2_approx(fmaf(q, -0.72134752044448170f, sb.w)));
+        } else {
+            float pq = ORDER == 1 ? sd.x : ORDER == 2 ? sd.y : sd.z;
+            if (ORDER >= 3) pq = fmaf(pq, q, sd.y);
+            if (ORDER >= 2) pq = fmaf(pq, q, sd.x);
+            alpha = fminf(0.999f, fmaf(pq, q, sb.w));
+        }
+    } else {
+        // non-monotone kernel: full ReLU / piecewise semantics, guard on alpha
+        const KernelF32& kf = A.P.kf;
+        float pq = kf.c[kf.order];
+        for (int j = kf.order - 1; j >= 0; --j) pq = fmaf(pq, q, kf.c[j]);
+        if (kf.kind == PS_KERNEL_POLY_PIECEWISE && !(q < kf.first_root)) pq = 0.0f;
+        alpha = KIND == 0 ? fminf(0.999f, ex2_approx(fmaf(q, -0.72134752044448170f, sb.w)))
+                          : fminf(0.999f, fmaxf(sb.w * pq, 0.0f)); // K0 = o here
+        if (alpha < A.P.eps_f - sb.y) return;
+        if (alpha < A.P.eps_f + sb.y) {
+            ++nexact;
+            if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, __float_as_uint(sd.w), gx, gy))
+                return;
+        }
+    }
+    p.eT += sc.x;
+    const float test_t = fmaf(-p.T, alpha, p.T);
+    const float fl = A.P.floor_f;
+    if (test_t < fmaf(fl, p.eT, fl)) {
+        if (test_t < fmaf(-fl, p.eT, fl)) {
+            if (COUNT) p.term = static_cast<uint32_t>(jpos);
+        } else {
+            p.flagged = true;
+        }
+        p.x = kNaNf; // finished
+        return;
+    }
+    const float w = alpha * p.T;
+    p.r = fmaf(sc.y, w, p.r);
+    p.g = fmaf(sc.z, w, p.g);
+    p.b = fmaf(sc.w, w, p.b);
+    p.T = test_t;
+    if (COUNT) ++p.nbl;
+}
+
+template <int KIND, int ORDER, int MODE, bool COUNT>
+__global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
+    __shared__ float4 sA[kB16];
+    __shared__ float4 sB[kB16];
+    __shared__ float4 sC[kB16];
+    __shared__ float4 sD[kB16];
+    __shared__ float4 sE[kB16];
+
+    const FrameParams& P = A.P;
+    const int tile = blockIdx.x;
+    const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
+    const int W = P.cam.width, H = P.cam.height;
+    const int px0 = tx * 16, py0 = ty * 16;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int lx = t & 7, ly = (warp << 2) + (lane >> 3);
+    const int gy = py0 + ly;
+    const float yc = ly + 0.5f;
+    // this warp's rows of pixel centres, for the culling test
+    const float wy_lo = (warp << 2) + 0.5f, wy_hi = (warp << 2) + 3.5f;
+    Px p0{(gy < H && px0 + lx < W) ? lx + 0.5f : kNaNf, 1.f, 0.f, 0.f, 0.f, 0.f, 0xffffffffu, 0u, false};
+    Px p1{(gy < H && px0 + lx + 8 < W) ? lx + 8.5f : kNaNf, 1.f, 0.f, 0.f, 0.f, 0.f, 0xffffffffu, 0u, false};
+    const bool in0 = p0.x == p0.x, in1 = p1.x == p1.x;
+    uint32_t nexact = 0;
+    const float c0 = P.kf.c[0], c1 = P.kf.c[1], c2 = P.kf.c[2], c3 = P.kf.c[3];
+
+    const uint2 range = A.ranges[tile];
+    const int L = static_cast<int>(range.y - range.x);
+    double2 pm = make_double2(0.0, 0.0);
+    float4 pb0 = make_float4(0.f, 0.f, 0.f, -1.f), pb1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 pb2 = make_float2(0.f, 0.f);
+    uint32_t pi = 0;
+    if (t < L) {
+        pi = A.pval[range.x + t];
+        pm = A.mean2d[pi];
+        pb0 = A.bl0[pi];
+        pb1 = A.bl1[pi];
+        pb2 = A.bl2[pi];
+    }
+    for (int base = 0; base < L; base += kB16) {
+        const bool live = (p0.x == p0.x) || (p1.x == p1.x);
+        if (__syncthreads_count(live) == 0) break;
+        {   // stage the record prefetched for this batch
+            const float mx = static_cast<float>(pm.x - px0), my = static_cast<float>(pm.y - py0);
+            const float Aq = pb0.x, beta = pb0.y, gamma = pb0.z, qhi = pb0.w;
+            sA[t] = make_float4(mx, my, Aq, beta);
+            const float o = pb1.y;
+            float K0 = o, K1 = 0.f, K2 = 0.f, K3 = 0.f;
+            if (KIND == 1 && MODE == kQuadricThreshold) {
+                K0 = o * c0; K1 = o * c1; K2 = o * c2; K3 = o * c3;
+            }
+            sB[t] = make_float4(gamma, qhi, pb1.x, K0);
+            sC[t] = make_float4(pb1.z, pb1.w, pb2.x, pb2.y);
+            sD[t] = make_float4(K1, K2, K3, __uint_as_float(pi));
+            // extent of {q <= q_hi}: |x - mx| <= sqrt(q_hi (beta^2/gamma + 1/A)), |y - my| <= sqrt(q_hi / gamma)
+            // (evaluated at q_hi + 2 Gq, Gq = (q_hi - q_lo)/2, so a culled pixel has q_fp32 > q_hi)
+            const float qb = qhi + (qhi - pb1.x);
+            float hx = sqrtf(qb * (beta * beta / gamma + 1.0f / Aq));
+            float hy = sqrtf(qb / gamma);
+            hx = hx * 1.001f + 1e-3f;
+            hy = hy * 1.001f + 1e-3f;
+            if (MODE != kQuadricThreshold || !(qhi < 3.0e38f)) { hx = INFINITY; hy = INFINITY; }
+            if (!(qhi >= 0.f)) { hx = -1.f; hy = -1.f; } // never reaches epsilon (or NaN)
+            sE[t] = make_float4(mx - hx, mx + hx, my - hy, my + hy);
+        }
+        __syncthreads();
+        const int nb = base + kB16;
+        if (nb + t < L) { // prefetch the next batch while this one is blended
+            pi = A.pval[range.x + nb + t];
+            pm = A.mean2d[pi];
+            pb0 = A.bl0[pi];
+            pb1 = A.bl1[pi];
+            pb2 = A.bl2[pi];
+        }
+        const int cnt = min(kB16, L - base);
+        if (!__any_sync(0xffffffffu, live)) continue;
+#pragma unroll
+        for (int g = 0; g < kB16 / 32; ++g) {
+            const int k0 = g * 32;
+            if (k0 >= cnt) break;
+            // warp culling: splats whose box misses this warp's 16x4 strip
+            const float4 e = sE[k0 + lane];
+            const bool hit = (k0 + lane < cnt) && e.x <= 15.5f && e.y >= 0.5f && e.z <= wy_hi && e.w >= wy_lo;
+            uint32_t m = __ballot_sync(0xffffffffu, hit);
+            while (m) {
+                const int k = k0 + __ffs(m) - 1;
+                m &= m - 1;
+                const float4 a = sA[k];
+                const float4 b = sB[k];
+                const float dy = yc - a.y;
+                const float mrow = fmaf(-a.w, dy, a.x);
+                const float R = b.x * dy * dy;
+                const float u0 = p0.x - mrow, u1 = p1.x - mrow;
+                const float q0 = fmaf(a.z * u0, u0, R);
+                const float q1 = fmaf(a.z * u1, u1, R);
+                const bool h0 = q0 <= b.y, h1 = q1 <= b.y;
+                if (h0 || h1) {
+                    const float4 c = sC[k];
+                    const float4 d = sD[k];
+                    if (h0) blend_px<KIND, ORDER, MODE, COUNT>(p0, q0, b, c, d, A, px0 + lx, gy, base + k, nexact);
+                    if (h1) blend_px<KIND, ORDER, MODE, COUNT>(p1, q1, b, c, d, A, px0 + lx + 8, gy, base + k, nexact);
+                }
+            }
+        }
+    }
+
+    unsigned long long ev = 0, bl = 0;
+    auto finish = [&](Px& p, bool inside, int gx) {
+        if (!inside) return;
+        const size_t pix = static_cast<size_t>(gy) * W + gx;
+        A.out_rgb[3 * pix + 0] = p.r;
+        A.out_rgb[3 * pix + 1] = p.g;
+        A.out_rgb[3 * pix + 2] = p.b;
+        A.out_t[pix] = p.T;
+        if (p.flagged) {
+            const unsigned long long slot = atomicAdd(&A.ctr->replay_px, 1ull);
+            A.flags[slot] = static_cast<uint32_t>(pix);
+        } else if (COUNT) {
+            ev += p.term != 0xffffffffu ? p.term + 1u : static_cast<unsigned>(L);
+            bl += p.nbl;
+        }
+    };
+    finish(p0, in0, px0 + lx);
+    finish(p1, in1, px0 + lx + 8);
+    unsigned long long ex = nexact;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ev += __shfl_xor_sync(0xffffffffu, ev, o);
+        bl += __shfl_xor_sync(0xffffffffu, bl, o);
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+    }
+    if (lane == 0) {
+        if (ev) atomicAdd(&A.ctr->evals, ev);
+        if (bl) atomicAdd(&A.ctr->blended, bl);
+        if (ex) atomicAdd(&A.ctr->exact_evals, ex);
+    }
+}
+
+template <int KIND, int ORDER, int MODE>
+void launch16(const BlendArgs& a, int n_tiles, bool count, cudaStream_t st) {
+    if (count) k_blend16<KIND, ORDER, MODE, true><<<n_tiles, 128, 0, st>>>(a);
+    else k_blend16<KIND, ORDER, MODE, false><<<n_tiles, 128, 0, st>>>(a);
+}
+
+template <int MODE>
+void launch16_kind(const BlendArgs& a, int n_tiles, bool count, cudaStream_t st) {
+    const KernelF32& kf = a.P.kf;
+    if (kf.kind == PS_KERNEL_EXPONENTIAL) launch16<0, 1, MODE>(a, n_tiles, count, st);
+    else if (kf.order == 1) launch16<1, 1, MODE>(a, n_tiles, count, st);
+    else if (kf.order == 2) launch16<1, 2, MODE>(a, n_tiles, count, st);
+    else launch16<1, 3, MODE>(a, n_tiles, count, st);
+}
+
 template <int KIND, int MODE>
 void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, cudaStream_t st) {
     if (count) k_blend<KIND, MODE, true><<<n_tiles, nt, smem, st>>>(a);
@@ -248,6 +478,11 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     if (n_tiles == 0) return 0;
     cudaMemcpyToSymbolAsync(c_exact_kernel, &P.cfg.kernel, sizeof(ps_kernel), 0, cudaMemcpyHostToDevice, st);
     cudaMemcpyToSymbolAsync(c_exact_eps, &P.cfg.epsilon, sizeof(double), 0, cudaMemcpyHostToDevice, st);
+    if (ts == 16) {
+        if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, st);
+        else launch16_kind<kAlphaThreshold>(a, n_tiles, count_work, st);
+        return 1;
+    }
     const bool expk = P.kf.kind == PS_KERNEL_EXPONENTIAL;
     if (P.threshold_mode == kQuadricThreshold) {
         if (expk) launch_t<0, kQuadricThreshold>(a, n_tiles, nt, smem, count_work, st);

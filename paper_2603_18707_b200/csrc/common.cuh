@@ -21,6 +21,10 @@
 namespace ps {
 
 constexpr int kShPlanes = 12; // 48 floats = 16 coefficients x 3 channels, as float4
+// Per-tile atomic counters live one per 128-byte L2 line: hot (central) tiles
+// take ~1e3 atomics each, and packed counters would serialise a whole row of
+// tiles on one L2 slice.
+constexpr int kCounterStride = 32;
 
 struct SceneDev {
     int64_t n = 0;
@@ -44,7 +48,11 @@ struct DevCounters {
     unsigned int error;              // first ps_status raised on device (0 = none)
     unsigned int error_index;        // splat index that raised it
     unsigned int pairs_total;        // P as computed by the count scan
-    unsigned int pad;
+    unsigned int max_tile_len;       // longest per-tile list (K2)
+    unsigned long long key_min;      // complement of the min / max fp64 depth bits (visible splats)
+    unsigned long long key_max;
+    unsigned int big_tiles;          // tiles with > 1024 pairs (listed in FrameDev::big_tiles)
+    unsigned int pad2;
 };
 
 // Per-splat frame arrays (indexed by original splat index).
@@ -59,6 +67,7 @@ struct FrameDev {
     double2* conic_ab = nullptr;        // fp64 (a, b)
     double2* conic_cq = nullptr;        // fp64 (c, culling quadric root incl. slack)
     ushort4* rect = nullptr;            // inclusive tile rect (x0, y0, x1, y1)
+    unsigned long long* tmask = nullptr; // tight-test bits over the rect (row-major), rect <= 64 tiles
     double* opacity_eff = nullptr;      // fp64 opacity_eff
     float4* bl0 = nullptr;              // fp32 blend record: A, beta, gamma, q_hi
     float4* bl1 = nullptr;              //   q_lo, o (or log2 o), eT, color r
@@ -70,6 +79,8 @@ struct FrameDev {
     uint32_t* pval = nullptr;
     uint32_t* pval_alt = nullptr;
     uint2* ranges = nullptr;            // per tile [start, end)
+    uint32_t* big_tiles = nullptr;      // ids of tiles with > 1024 pairs
+    uint32_t* tile_count = nullptr;     // pairs per tile (K1c red.add), then the K3 cursors; stride kCounterStride
     uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
     double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)
 };

@@ -122,7 +122,7 @@ size_t frame_bytes(int64_t n) {
     size_t s = 0;
     s += 2 * al(8 * n) + 2 * al(4 * n) + 2 * al(4 * n); // key, key_alt, val, val_alt, tcount, offset
     s += 3 * al(16 * n);                                 // mean2d, conic_ab, conic_cq
-    s += al(8 * n) + al(8 * n);                          // rect, opacity_eff
+    s += al(8 * n) + al(8 * n) + al(8 * n);              // rect, opacity_eff, tmask
     s += 2 * al(16 * n) + al(8 * n);                     // bl0, bl1, bl2
     return s;
 }
@@ -145,6 +145,7 @@ int ensure_frame(ps_ctx* c, int64_t n) {
     c->f.conic_ab = carve<double2>(p, cap);
     c->f.conic_cq = carve<double2>(p, cap);
     c->f.rect = carve<ushort4>(p, cap);
+    c->f.tmask = carve<unsigned long long>(p, cap);
     c->f.opacity_eff = carve<double>(p, cap);
     c->f.bl0 = carve<float4>(p, cap);
     c->f.bl1 = carve<float4>(p, cap);
@@ -206,9 +207,15 @@ int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
     }
     if (n_tiles > c->tiles_cap) {
         if (c->f.ranges) cudaFree(c->f.ranges);
+        if (c->f.tile_count) cudaFree(c->f.tile_count);
+        if (c->f.big_tiles) cudaFree(c->f.big_tiles);
         c->f.ranges = nullptr;
+        c->f.tile_count = nullptr;
+        c->f.big_tiles = nullptr;
         c->tiles_cap = 0;
         CTX_TRY(c, cudaMalloc(&c->f.ranges, sizeof(uint2) * n_tiles));
+        CTX_TRY(c, cudaMalloc(&c->f.tile_count, sizeof(uint32_t) * kCounterStride * n_tiles));
+        CTX_TRY(c, cudaMalloc(&c->f.big_tiles, sizeof(uint32_t) * n_tiles));
         c->tiles_cap = n_tiles;
     }
     return PS_OK;
@@ -301,26 +308,39 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     int launches = 0;
     cudaStream_t strm = c->stream;
     CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
+    if (req.mode != Mode::Prepare)
+        CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * kCounterStride * n_tiles, strm));
+    else
+        f.tile_count = nullptr;
     record(c, 0);
+    // K1: preprocess (+ tight pair count per tile)
     launch_preprocess(s->dev, P, f, c->d_ctr, strm);
     launches += n > 0;
     record(c, 1);
-    // K2: stable radix sort of the fp64 depth bits (positive doubles order as
-    // their bit patterns); culled splats carry ~0 and sort last.
-    bool oalt = radix_sort_u64(f.key, f.key_alt, f.val, f.val_alt, nullptr, n, 0, 64, c->radix_scratch,
-                               strm, &launches);
-    const uint32_t* order = oalt ? f.val_alt : f.val;
+    const uint32_t* order = nullptr;
+    if (req.mode == Mode::Prepare) {
+        // prepare_splats needs the global (depth, index) order: stable radix
+        // sort of the fp64 depth bits (culled splats carry ~0 and sort last)
+        bool oalt = radix_sort_u64(f.key, f.key_alt, f.val, f.val_alt, nullptr, n, 0, 64, c->radix_scratch,
+                                   strm, &launches);
+        order = oalt ? f.val_alt : f.val;
+        res.order_in_alt = oalt;
+        scan_gathered_counts(f.tcount, order, f.offset, n, &c->d_ctr->pairs_total, c->scan_scratch, strm,
+                             &launches);
+    } else {
+        // K1c + K2: pairs per tile, then tile ranges + bucket cursors
+        launch_count_tiles(f, P, n, strm);
+        launch_tile_scan(f.tile_count, f.ranges, n_tiles, c->d_ctr, f.big_tiles, strm);
+        launches += 2;
+    }
     record(c, 2);
-    // K3a: exclusive scan of tight counts in depth order
-    scan_gathered_counts(f.tcount, order, f.offset, n, &c->d_ctr->pairs_total, c->scan_scratch, strm,
-                         &launches);
     CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
     CTX_TRY(c, cudaStreamSynchronize(strm));
     CTX_TRY(c, cudaGetLastError());
+    record(c, 3);
     res.ctr = *c->h_ctr;
     res.visible = static_cast<int64_t>(res.ctr.visible);
     res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
-    res.order_in_alt = oalt;
     if (res.ctr.error) {
         char buf[256];
         std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
@@ -338,20 +358,34 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
 
     if ((st = ensure_pairs(c, res.pairs)) != PS_OK) return st;
     f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
-    // K3b: duplicate-with-keys in depth order
-    launch_duplicate(f, P, order, n, strm);
-    launches += n > 0;
-    record(c, 3);
-    // K4: stable sort of pairs by tile id (depth order is preserved within a tile)
-    bool palt = radix_sort_u32(f.pkey, f.pkey_alt, f.pval, f.pval_alt, nullptr, res.pairs, 0,
-                               bits_for(n_tiles), c->radix_scratch, strm, &launches);
-    res.pairs_in_alt = palt;
-    const uint32_t* skeys = palt ? f.pkey_alt : f.pkey;
-    const uint32_t* svals = palt ? f.pval_alt : f.pval;
-    record(c, 4);
-    // K5: tile ranges
-    launch_ranges(skeys, nullptr, res.pairs, f.ranges, n_tiles, strm, &launches);
-    record(c, 5);
+    const uint32_t* svals = f.pval;
+    if (res.ctr.max_tile_len <= 16384u) {
+        // K3: scatter splat indices into per-tile buckets
+        launch_duplicate_buckets(f, P, n, strm);
+        launches += n > 0;
+        record(c, 4);
+        // K4: exact (depth, index) order inside every bucket
+        launch_tile_sort(f, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+        record(c, 5);
+    } else {
+        // Fallback for tiles longer than one CTA's shared memory: global stable
+        // radix sort by depth, duplicate in depth order, stable sort by tile.
+        bool oalt = radix_sort_u64(f.key, f.key_alt, f.val, f.val_alt, nullptr, n, 0, 64, c->radix_scratch,
+                                   strm, &launches);
+        order = oalt ? f.val_alt : f.val;
+        scan_gathered_counts(f.tcount, order, f.offset, n, &c->d_ctr->pairs_total, c->scan_scratch, strm,
+                             &launches);
+        launch_duplicate(f, P, order, n, strm);
+        launches += n > 0;
+        record(c, 4);
+        bool palt = radix_sort_u32(f.pkey, f.pkey_alt, f.pval, f.pval_alt, nullptr, res.pairs, 0,
+                                   bits_for(n_tiles), c->radix_scratch, strm, &launches);
+        res.pairs_in_alt = palt;
+        const uint32_t* skeys = palt ? f.pkey_alt : f.pkey;
+        svals = palt ? f.pval_alt : f.pval;
+        launch_ranges(skeys, nullptr, res.pairs, f.ranges, n_tiles, strm, &launches);
+        record(c, 5);
+    }
     if (req.mode == Mode::TileLists) {
         CTX_TRY(c, cudaStreamSynchronize(strm));
         CTX_TRY(c, cudaGetLastError());
@@ -380,10 +414,9 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     c->stats.exact_alpha_evals = res.ctr.exact_evals;
     c->stats.kernel_launches = launches;
     if (c->timing) {
-        const int map[PS_STAGE_COUNT][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}};
         for (int k = 0; k < PS_STAGE_COUNT; ++k) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, c->ev[map[k][0]], c->ev[map[k][1]]);
+            cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
             c->stats.stage_ms[k] = ms;
         }
     }
@@ -539,7 +572,7 @@ void ps_ctx_destroy(ps_ctx* c) {
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
     void* bufs[] = {c->n_block, c->p_block, c->radix_scratch, c->scan_scratch, c->img_rgb, c->img_t,
-                    c->f.flags, c->f.ranges, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage};
+                    c->f.flags, c->f.ranges, c->f.tile_count, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);

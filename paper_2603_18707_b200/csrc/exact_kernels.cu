@@ -110,7 +110,8 @@ __device__ void blend_record(double a, double b, double c, double o, double mx, 
         double dmx = e32 * (X + ts), dmy = e32 * (D + ts);
         double ddx = dmx + e32 * X, ddy = dmy + e32 * D;
         double gam_rel = e32 + 4.0 * e64 * (c + b * b / a) / gamma;
-        double du = ddx + ab_ * ddy + e32 * ab_ * D + e32 * (U + X);
+        // u is formed either as (dx + beta dy) or as x - (mx - beta dy); bound both
+        double du = 2.0 * dmx + ddx + ab_ * ddy + 2.0 * e32 * ab_ * D + e32 * (U + X);
         double dr = qb * (2.0 * e32 + gam_rel) + 2.0 * gamma * D * ddy;
         double dau = qb * 3.0 * e32 + 2.0 * a * U * du;
         double dq = e32 * qb + dau + dr;
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
                                                     DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
+    unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
     if (i < s.n) {
         unsigned long long key = ~0ull;
         uint32_t cnt = 0;
@@ -193,11 +195,19 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
                     visible = 1;
                     coarse = static_cast<unsigned long long>(r[2] - r[0] + 1) *
                              static_cast<unsigned long long>(r[3] - r[1] + 1);
+                    unsigned long long mask = 0ull;
+                    int bit = 0;
                     for (int ty = r[1]; ty <= r[3]; ++ty)
-                        for (int tx = r[0]; tx <= r[2]; ++tx)
-                            cnt += tight_tile_test(pr.conic, pr.mx, pr.my, qroot, tx, ty, ts) ? 1u : 0u;
+                        for (int tx = r[0]; tx <= r[2]; ++tx, ++bit)
+                            if (tight_tile_test(pr.conic, pr.mx, pr.my, qroot, tx, ty, ts)) {
+                                ++cnt;
+                                if (bit < 64) mask |= 1ull << bit;
+                            }
+                    f.tmask[i] = mask;
                     tight = cnt;
                     key = static_cast<unsigned long long>(__double_as_longlong(pr.depth));
+                    kmin_inv = ~key;
+                    kmax = key;
                     f.mean2d[i] = make_double2(pr.mx, pr.my);
                     f.conic_ab[i] = make_double2(pr.conic.xx, pr.conic.xy);
                     f.conic_cq[i] = make_double2(pr.conic.yy, qroot);
@@ -237,6 +247,15 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
         f.key[i] = key;
         f.val[i] = static_cast<uint32_t>(i);
         f.tcount[i] = cnt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin_inv = max(kmin_inv, __shfl_xor_sync(0xffffffffu, kmin_inv, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && kmax) {
+        atomicMax(&ctr->key_min, kmin_inv);
+        atomicMax(&ctr->key_max, kmax);
     }
     frustum = warp_sum_u64(frustum);
     coarse = warp_sum_u64(coarse);
@@ -278,54 +297,132 @@ __global__ void __launch_bounds__(256) k_duplicate(FrameDev f, FrameParams P, co
             }
 }
 
+// Tight tiles of splat i as tile ids, from the K1 bitmask (rect <= 64 tiles) or
+// by re-running the exact tight test (larger rects). Calls fn(tile) in the
+// rect's row-major order.
+template <class Fn>
+__device__ __forceinline__ void for_each_tight_tile(const FrameDev& f, const FrameParams& P, int64_t i, Fn&& fn) {
+    const ushort4 rc = f.rect[i];
+    const int w = rc.z - rc.x + 1, h = rc.w - rc.y + 1;
+    if (w * h <= 64) {
+        unsigned long long m = f.tmask[i];
+        while (m) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            fn((rc.y + b / w) * P.tiles_x + rc.x + b % w);
+        }
+        return;
+    }
+    const double2 mm = f.mean2d[i];
+    const double2 ab = f.conic_ab[i];
+    const double2 cq = f.conic_cq[i];
+    const Sym2 cn{ab.x, ab.y, cq.x};
+    const int ts = P.cfg.tile_size;
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+        for (int tx = rc.x; tx <= rc.z; ++tx)
+            if (tight_tile_test(cn, mm.x, mm.y, cq.y, tx, ty, ts)) fn(ty * P.tiles_x + tx);
+}
+
+// K1c: pairs per tile (red.add; result unused).
+__global__ void __launch_bounds__(256) k_count_tiles(FrameDev f, FrameParams P, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n || f.tcount[i] == 0) return;
+    for_each_tight_tile(f, P, i, [&](int t) { atomicAdd(&f.tile_count[t * kCounterStride], 1u); });
+}
+
+// K3 (bucketed): splat indices into per-tile buckets at atomically claimed
+// slots. The order inside a bucket is arbitrary; K4 sorts each bucket by the
+// reference's exact key.
+__global__ void __launch_bounds__(256) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n || f.tcount[i] == 0) return;
+    for_each_tight_tile(f, P, i, [&](int t) {
+        const uint32_t slot = atomicAdd(&f.tile_count[t * kCounterStride], 1u);
+        f.pval[slot] = static_cast<uint32_t>(i);
+    });
+}
+
 // ------------------------------------------------------------ K7 exact replay
-// One thread per flagged pixel: the reference's per-pixel loop in fp64
-// (raster.cpp:250-283), over the pixel's tile list. Colours are the same fp32
-// SH colours the fast path blends.
-__global__ void __launch_bounds__(128) k_replay(FrameDev f, FrameParams P, DevCounters* ctr,
+// One WARP per flagged pixel: the reference's per-pixel loop in fp64
+// (raster.cpp:250-283) over the pixel's tile list. The 32 lanes evaluate
+// alpha for 32 consecutive list entries at once (independent); the
+// transmittance chain, which is sequential, then runs over the accepted
+// fragments in list order with every lane holding the same (T, r, g, b), so
+// each operation happens in the reference's order and rounding. Colours are
+// the same fp32 SH colours the fast path blends.
+__global__ void __launch_bounds__(256) k_replay(FrameDev f, FrameParams P, DevCounters* ctr,
                                                 float* out_rgb, float* out_t, int count_work) {
     const unsigned long long n_flags = ctr->replay_px;
     const int W = P.cam.width;
     const int ts = P.cfg.tile_size;
-    for (unsigned long long slot = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-         slot < n_flags; slot += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long warp0 = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
+    const double eps = P.cfg.epsilon, floor_t = P.cfg.transmittance_floor;
+    for (unsigned long long slot = warp0; slot < n_flags; slot += nwarps) {
         const uint32_t pix = f.flags[slot];
         const int px = static_cast<int>(pix % W), py = static_cast<int>(pix / W);
         const int tile = (py / ts) * P.tiles_x + (px / ts);
         const uint2 range = f.ranges[tile];
         double trans = 1.0, r = 0.0, g = 0.0, b = 0.0;
         unsigned long long evals = 0, blended = 0;
-        for (uint32_t j = range.x; j < range.y; ++j) {
-            const uint32_t i = f.pval[j];
-            const double2 m = f.mean2d[i];
-            const double2 ab = f.conic_ab[i];
-            const double2 cq = f.conic_cq[i];
-            const double o = f.opacity_eff[i];
-            const double dx = px + 0.5 - m.x;
-            const double dy = py + 0.5 - m.y;
-            const double q = ab.x * dx * dx + 2.0 * ab.y * dx * dy + cq.x * dy * dy;
-            ++evals;
-            const double alpha = std_min(0.999, o * eval_kernel(P.cfg.kernel, q));
-            if (alpha < P.cfg.epsilon) continue;
-            const double test_t = trans * (1.0 - alpha);
-            if (test_t < P.cfg.transmittance_floor) break;
-            const float4 b1 = f.bl1[i];
-            const float2 b2 = f.bl2[i];
-            const double w = alpha * trans;
-            r += static_cast<double>(b1.w) * w;
-            g += static_cast<double>(b2.x) * w;
-            b += static_cast<double>(b2.y) * w;
-            trans = test_t;
-            ++blended;
+        bool done = false;
+        for (uint32_t base = range.x; base < range.y && !done; base += 32) {
+            const uint32_t j = base + lane;
+            const bool valid = j < range.y;
+            double alpha = 0.0;
+            float cr = 0.f, cg = 0.f, cb = 0.f;
+            bool acc = false;
+            if (valid) {
+                const uint32_t i = f.pval[j];
+                const double2 m = f.mean2d[i];
+                const double2 ab = f.conic_ab[i];
+                const double2 cq = f.conic_cq[i];
+                const double o = f.opacity_eff[i];
+                const double dx = px + 0.5 - m.x;
+                const double dy = py + 0.5 - m.y;
+                const double q = ab.x * dx * dx + 2.0 * ab.y * dx * dy + cq.x * dy * dy;
+                alpha = std_min(0.999, o * eval_kernel(P.cfg.kernel, q));
+                acc = !(alpha < eps);
+                if (acc) {
+                    const float4 b1 = f.bl1[i];
+                    const float2 b2 = f.bl2[i];
+                    cr = b1.w; cg = b2.x; cb = b2.y;
+                }
+            }
+            uint32_t mask = __ballot_sync(0xffffffffu, acc);
+            const uint32_t nvalid = min(32u, range.y - base);
+            int stop = -1;
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const double a = __shfl_sync(0xffffffffu, alpha, src);
+                const double test_t = trans * (1.0 - a);
+                if (test_t < floor_t) { stop = src; break; }
+                const double w = a * trans;
+                r += static_cast<double>(__shfl_sync(0xffffffffu, cr, src)) * w;
+                g += static_cast<double>(__shfl_sync(0xffffffffu, cg, src)) * w;
+                b += static_cast<double>(__shfl_sync(0xffffffffu, cb, src)) * w;
+                trans = test_t;
+                ++blended;
+            }
+            if (stop >= 0) {
+                evals += static_cast<unsigned long long>(stop) + 1;
+                done = true;
+            } else {
+                evals += nvalid;
+            }
         }
-        out_rgb[3ull * pix + 0] = static_cast<float>(r);
-        out_rgb[3ull * pix + 1] = static_cast<float>(g);
-        out_rgb[3ull * pix + 2] = static_cast<float>(b);
-        out_t[pix] = static_cast<float>(trans);
-        if (f.replay_vals) f.replay_vals[slot] = make_double4(r, g, b, trans);
-        if (count_work) {
-            atomicAdd(&ctr->evals, evals);
-            atomicAdd(&ctr->blended, blended);
+        if (lane == 0) {
+            out_rgb[3ull * pix + 0] = static_cast<float>(r);
+            out_rgb[3ull * pix + 1] = static_cast<float>(g);
+            out_rgb[3ull * pix + 2] = static_cast<float>(b);
+            out_t[pix] = static_cast<float>(trans);
+            if (f.replay_vals) f.replay_vals[slot] = make_double4(r, g, b, trans);
+            if (count_work) {
+                atomicAdd(&ctr->evals, evals);
+                atomicAdd(&ctr->blended, blended);
+            }
         }
     }
 }
@@ -345,9 +442,21 @@ void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* o
     k_duplicate<<<blocks, 256, 0, st>>>(f, P, order, n);
 }
 
+void launch_count_tiles(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st) {
+    if (n == 0) return;
+    const int blocks = static_cast<int>((n + 255) / 256);
+    k_count_tiles<<<blocks, 256, 0, st>>>(f, P, n);
+}
+
+void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st) {
+    if (n == 0) return;
+    const int blocks = static_cast<int>((n + 255) / 256);
+    k_duplicate_buckets<<<blocks, 256, 0, st>>>(f, P, n);
+}
+
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
                    float* out_t, bool count_work, int sm_count, cudaStream_t st) {
-    k_replay<<<sm_count * 2, 128, 0, st>>>(f, P, ctr, out_rgb, out_t, count_work ? 1 : 0);
+    k_replay<<<sm_count * 4, 256, 0, st>>>(f, P, ctr, out_rgb, out_t, count_work ? 1 : 0);
 }
 
 } // namespace ps

@@ -13,6 +13,8 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
                        cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
                       cudaStream_t st);
+void launch_count_tiles(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
+void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
                    float* out_t, bool count_work, int sm_count, cudaStream_t st);
 
@@ -38,6 +40,14 @@ void scan_gathered_counts(const uint32_t* tcount, const uint32_t* order, uint32_
 // per-tile [start, end) over sorted tile keys (K5)
 void launch_ranges(const uint32_t* keys, const uint32_t* d_n, int64_t n_cap, uint2* ranges,
                    int n_tiles, cudaStream_t st, int* launches);
+
+// binning.cu — per-tile buckets (K2 tile scan, K4 per-tile exact depth sort)
+void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
+                      cudaStream_t st);
+// sorts every bucket with 1 < length <= max_items (shared memory); returns false
+// when max_items exceeds what one CTA can hold (caller falls back)
+bool launch_tile_sort(const FrameDev& f, int n_tiles, uint32_t max_len, const DevCounters* d_ctr, cudaStream_t st,
+                      int* launches);
 
 // blend.cu (K6)
 struct BlendOut {
