@@ -163,6 +163,8 @@ void* ps_ctx_stream(ps_ctx* ctx);
 /* FP32 FFMA issue-rate microbenchmark (TFLOP/s, FFMA = 2 flops): the measured
  * roofline denominator of the FP32-bound blend kernel. */
 int ps_measure_fp32_peak(ps_ctx* ctx, double* tflops);
+/* fp64 DFMA issue-rate microbenchmark (TFLOP/s): denominator for the fp64 preprocess. */
+int ps_measure_fp64_peak(ps_ctx* ctx, double* tflops);
 
 /* ---------------------------------------------------------------- scenes
  * A scene is a device-resident SoA copy of the splats (fp64 geometry, fp32 SH),

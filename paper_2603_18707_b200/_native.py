@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolyspla
 EXPORTS = (
     "ps_version", "ps_abi_version", "ps_device_count", "ps_ctx_create", "ps_ctx_destroy",
     "ps_last_error", "ps_ctx_set_timing", "ps_last_stats", "ps_ctx_synchronize", "ps_ctx_stream",
-    "ps_measure_fp32_peak",
+    "ps_measure_fp32_peak", "ps_measure_fp64_peak",
     "ps_scene_create_aos", "ps_scene_create_soa", "ps_scene_update_soa", "ps_scene_size",
     "ps_scene_destroy", "ps_render", "ps_render_views", "ps_render_splats", "ps_count_pairs",
     "ps_prepare", "ps_tile_lists", "ps_make_polynomial_kernel", "ps_make_exponential_kernel",
@@ -45,6 +45,7 @@ def _declare(L) -> None:
         "ps_ctx_synchronize": (C.c_int, [vp]),
         "ps_ctx_stream": (vp, [vp]),
         "ps_measure_fp32_peak": (C.c_int, [vp, dp]),
+        "ps_measure_fp64_peak": (C.c_int, [vp, dp]),
         "ps_scene_create_aos": (C.c_int, [vp, dp, i64, P(vp)]),
         "ps_scene_create_soa": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, C.c_int, P(vp)]),
         "ps_scene_update_soa": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int]),

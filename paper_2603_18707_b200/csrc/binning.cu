@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
     uint32_t carry = 0, mx = 0;
     for (int base = 0; base < n_tiles; base += kScanThreads) {
         const int t = base + threadIdx.x;
-        const uint32_t v = t < n_tiles ? count[static_cast<size_t>(t) * kCounterStride] : 0u;
+        const uint32_t v = t < n_tiles ? count[static_cast<size_t>(t)] : 0u;
         mx = max(mx, v);
         uint32_t x = v;
 #pragma unroll
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
         const uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
         if (t < n_tiles) {
             ranges[t] = make_uint2(excl, excl + v);
-            count[static_cast<size_t>(t) * kCounterStride] = excl; // becomes the K3 cursor
+            count[static_cast<size_t>(t)] = excl; // becomes the K3 cursor
             if (v > 1024u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
         }
         carry += wsum[31];
@@ -91,7 +91,7 @@ struct TileSortSmem {
 
 template <int THREADS, int ROUNDS>
 __device__ void sort_one_tile(const uint2 r, uint32_t* __restrict__ pval, const unsigned long long* __restrict__ key,
-                              uint32_t* smem) {
+                              const uint32_t* __restrict__ orig, uint32_t* smem) {
     constexpr int WARPS = THREADS / 32;
     constexpr int CAP = THREADS * ROUNDS;
     uint32_t* kbuf = smem;                                     // [2][CAP]
@@ -236,7 +236,7 @@ __device__ void sort_one_tile(const uint2 r, uint32_t* __restrict__ pval, const 
                 while (b >= j) {
                     const uint32_t vb = vs[b];
                     const unsigned long long kb = key[vb];
-                    if (kb < ka || (kb == ka && vb < va)) break;
+                    if (kb < ka || (kb == ka && orig[vb] < orig[va])) break;
                     vs[b + 1] = vb;
                     --b;
                 }
@@ -264,7 +264,8 @@ __device__ void sort_one_tile(const uint2 r, uint32_t* __restrict__ pval, const 
                     const int ix = i + jj;
                     const unsigned long long ka = fk[i], kb = fk[ix];
                     const uint32_t va = vs[i], vb = vs[ix];
-                    const bool gt = ka > kb || (ka == kb && va > vb);
+                    const bool gt = ka > kb || (ka == kb && (va == 0xffffffffu ? 0xffffffffu : orig[va]) >
+                                                                   (vb == 0xffffffffu ? 0xffffffffu : orig[vb]));
                     if (gt == ((i & k) == 0)) { fk[i] = kb; fk[ix] = ka; vs[i] = vb; vs[ix] = va; }
                 }
                 __syncthreads();
@@ -276,18 +277,20 @@ __device__ void sort_one_tile(const uint2 r, uint32_t* __restrict__ pval, const 
 // Small buckets (length <= CAP): one CTA per tile over the whole grid.
 template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_small(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
-                                                             const unsigned long long* __restrict__ key) {
+                                                             const unsigned long long* __restrict__ key,
+                                                             const uint32_t* __restrict__ orig) {
     extern __shared__ uint32_t smem[];
     const uint2 r = ranges[blockIdx.x];
     const int L = static_cast<int>(r.y - r.x);
     if (L <= 1 || L > THREADS * ROUNDS) return;
-    sort_one_tile<THREADS, ROUNDS>(r, pval, key, smem);
+    sort_one_tile<THREADS, ROUNDS>(r, pval, key, orig, smem);
 }
 
 // Large buckets: grid-stride over the device-built list of long tiles.
 template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
                                                             const unsigned long long* __restrict__ key,
+                                                            const uint32_t* __restrict__ orig,
                                                             const uint32_t* __restrict__ list, const uint32_t* count,
                                                             int min_len_exclusive) {
     extern __shared__ uint32_t smem[];
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
         const uint2 r = ranges[list[q]];
         const int L = static_cast<int>(r.y - r.x);
         if (L <= min_len_exclusive || L > THREADS * ROUNDS) continue;
-        sort_one_tile<THREADS, ROUNDS>(r, pval, key, smem);
+        sort_one_tile<THREADS, ROUNDS>(r, pval, key, orig, smem);
         __syncthreads();
     }
 }
@@ -311,24 +314,24 @@ void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCount
 // Bucket length <= 1024: 128 threads per tile over all tiles; longer buckets
 // (listed by k_tile_scan) by 512-thread (<= 4096) and 1024-thread (<= 16384)
 // CTAs. Longer than 16384: returns false (caller falls back).
-bool launch_tile_sort(const FrameDev& f, int n_tiles, uint32_t max_len, const DevCounters* d_ctr, cudaStream_t st,
-                      int* launches) {
+bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint32_t max_len,
+                      const DevCounters* d_ctr, cudaStream_t st, int* launches) {
     if (max_len <= 1 || n_tiles == 0) return true;
     if (max_len > 16384u) return false;
     using S1 = TileSortSmem<128, 8>;
-    k_tile_sort_small<128, 8><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key);
+    k_tile_sort_small<128, 8><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key, orig);
     if (launches) *launches += 1;
     if (max_len > 1024u) {
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-        k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, f.big_tiles,
+        k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 1024);
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 16>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, f.big_tiles,
+        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096);
         if (launches) *launches += 1;
     }

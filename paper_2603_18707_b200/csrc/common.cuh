@@ -1,7 +1,11 @@
 // common.cuh — device data layout shared by the rasterizer stages.
 //
 // HBM layout (all arrays indexed by the ORIGINAL splat index i unless noted):
-//   scene (uploaded once, ps_scene):  fp64 SoA mean_x/y/z, scale_x/y/z, rot_w/x/y/z,
+//   scene (uploaded once, ps_scene):  splats reordered along a 3D Morton curve (so a
+//                                     warp's splats are spatial neighbours; orig[]
+//                                     keeps the original index for the reference's
+//                                     tie-break and every output);
+//                                     fp64 SoA mean_x/y/z, scale_x/y/z, rot_w/x/y/z,
 //                                     opacity (88 B/splat) + SH as 12 float4 per splat
 //                                     sh4[i*12 + j] (the Splat3D coefficient order;
 //                                     192 B/splat at degree 3)
@@ -21,10 +25,7 @@
 namespace ps {
 
 constexpr int kShPlanes = 12; // 48 floats = 16 coefficients x 3 channels, as float4
-// Per-tile atomic counters live one per 128-byte L2 line: hot (central) tiles
-// take ~1e3 atomics each, and packed counters would serialise a whole row of
-// tiles on one L2 slice.
-constexpr int kCounterStride = 32;
+
 
 struct SceneDev {
     int64_t n = 0;
@@ -33,6 +34,7 @@ struct SceneDev {
     double* rot[4] = {nullptr, nullptr, nullptr, nullptr};
     double* opacity = nullptr;
     float4* sh4 = nullptr; // [n][kShPlanes]
+    uint32_t* orig = nullptr; // internal -> original splat index (Morton order at upload)
 };
 
 // Device counters / status words (one struct per context, zeroed per render).
@@ -80,7 +82,7 @@ struct FrameDev {
     uint32_t* pval_alt = nullptr;
     uint2* ranges = nullptr;            // per tile [start, end)
     uint32_t* big_tiles = nullptr;      // ids of tiles with > 1024 pairs
-    uint32_t* tile_count = nullptr;     // pairs per tile (K1c red.add), then the K3 cursors; stride kCounterStride
+    uint32_t* tile_count = nullptr;     // pairs per tile (K1a), then the K3 bucket cursors
     uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
     double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)
 };
@@ -106,6 +108,9 @@ struct FrameParams {
     int threshold_mode;     // ThresholdMode
     KernelF32 kf;           // blend kernel in fp32
     float eps_f, floor_f;
+    int bound_class;        // K1a specialisation (culling mode x bound kernel)
+    int blend_class;        // K1b specialisation (blend kernel)
+    double campos[3];       // Camera::position() (projection.hpp:29), computed on the host
 };
 
 #define PS_CUDA_TRY(expr)                                                  \

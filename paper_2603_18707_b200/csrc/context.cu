@@ -32,6 +32,8 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 int host_validate_config(const ps_config& c);
 int host_validate_camera(const ps_camera& c);
 int host_kernel_threshold_mode(const ps_kernel& k);
+int host_effective_terms(const ps_kernel& k);
+void host_camera_position(const ps_camera& cam, double out[3]);
 
 } // namespace ps
 
@@ -214,7 +216,7 @@ int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
         c->f.big_tiles = nullptr;
         c->tiles_cap = 0;
         CTX_TRY(c, cudaMalloc(&c->f.ranges, sizeof(uint2) * n_tiles));
-        CTX_TRY(c, cudaMalloc(&c->f.tile_count, sizeof(uint32_t) * kCounterStride * n_tiles));
+        CTX_TRY(c, cudaMalloc(&c->f.tile_count, sizeof(uint32_t) * n_tiles));
         CTX_TRY(c, cudaMalloc(&c->f.big_tiles, sizeof(uint32_t) * n_tiles));
         c->tiles_cap = n_tiles;
     }
@@ -284,6 +286,22 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     P.kf.first_root = static_cast<float>(cfg.kernel.first_root);
     P.eps_f = static_cast<float>(cfg.epsilon);
     P.floor_f = static_cast<float>(cfg.transmittance_floor);
+    host_camera_position(cam, P.campos);
+    {   // kernel specialisations (exact_kernels.cu BoundClass / BlendClass)
+        const ps_kernel& bk = cfg.has_culling_kernel ? cfg.culling_kernel : cfg.kernel;
+        if (cfg.culling_mode == PS_CULL_STOP_THE_POP) P.bound_class = 0;
+        else if (cfg.culling_mode == PS_CULL_ZERO_CROSSING) P.bound_class = 1;
+        else if (bk.kind == PS_KERNEL_EXPONENTIAL) P.bound_class = 2;
+        else {
+            const int nt = host_effective_terms(bk);
+            P.bound_class = nt == 2 ? 3 : nt == 3 ? 4 : nt == 4 ? 5 : 6;
+        }
+        if (cfg.kernel.kind == PS_KERNEL_EXPONENTIAL) P.blend_class = 0;
+        else {
+            const int nt = host_effective_terms(cfg.kernel);
+            P.blend_class = nt == 2 ? 1 : nt == 3 ? 2 : nt == 4 ? 3 : 4;
+        }
+    }
     const int n_tiles = P.tiles_x * P.tiles_y;
     const int64_t pix = static_cast<int64_t>(cam.width) * cam.height;
 
@@ -309,13 +327,13 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     cudaStream_t strm = c->stream;
     CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
     if (req.mode != Mode::Prepare)
-        CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * kCounterStride * n_tiles, strm));
+        CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * n_tiles, strm));
     else
         f.tile_count = nullptr;
     record(c, 0);
     // K1: preprocess (+ tight pair count per tile)
     launch_preprocess(s->dev, P, f, c->d_ctr, strm);
-    launches += n > 0;
+    launches += n > 0 ? 2 : 0;
     record(c, 1);
     const uint32_t* order = nullptr;
     if (req.mode == Mode::Prepare) {
@@ -328,10 +346,9 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         scan_gathered_counts(f.tcount, order, f.offset, n, &c->d_ctr->pairs_total, c->scan_scratch, strm,
                              &launches);
     } else {
-        // K1c + K2: pairs per tile, then tile ranges + bucket cursors
-        launch_count_tiles(f, P, n, strm);
+        // K2: tile ranges + bucket cursors from the per-tile counts (K1a)
         launch_tile_scan(f.tile_count, f.ranges, n_tiles, c->d_ctr, f.big_tiles, strm);
-        launches += 2;
+        launches += 1;
     }
     record(c, 2);
     CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
@@ -342,9 +359,11 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     res.visible = static_cast<int64_t>(res.ctr.visible);
     res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
     if (res.ctr.error) {
+        uint32_t orig_index = res.ctr.error_index;
+        cudaMemcpy(&orig_index, s->dev.orig + res.ctr.error_index, sizeof(uint32_t), cudaMemcpyDeviceToHost);
         char buf[256];
         std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
-                      res.ctr.error_index);
+                      orig_index);
         return set_err(c, static_cast<int>(res.ctr.error), buf);
     }
     if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
@@ -365,7 +384,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         launches += n > 0;
         record(c, 4);
         // K4: exact (depth, index) order inside every bucket
-        launch_tile_sort(f, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+        launch_tile_sort(f, s->dev.orig, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
         record(c, 5);
     } else {
         // Fallback for tiles longer than one CTA's shared memory: global stable
@@ -468,10 +487,13 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
     const int64_t n = s->n;
     if (n == 0) return PS_OK;
     const cudaMemcpyKind kind = memspace == PS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // means/scales/rotations arrive interleaved per splat (n x 3 / n x 4): copy
-    // them raw into a staging buffer (three large DMAs; full PCIe/C2C rate when
-    // the host buffers are pinned) and de-interleave into planes on the device.
-    const size_t stage_bytes = sizeof(double) * 10 * static_cast<size_t>(n);
+    // Stage the raw arrays (a few large DMAs; full link rate when the host
+    // buffers are pinned), order the splats along a Morton curve of their means,
+    // and gather them into the scene's SoA planes in that order.
+    const size_t geo = sizeof(double) * 11 * static_cast<size_t>(n);
+    const size_t shb = sizeof(float) * 48 * static_cast<size_t>(n);
+    const size_t sort_bytes = sizeof(uint32_t) * 4 * static_cast<size_t>(n) + radix_scratch_bytes(n) + 64;
+    const size_t stage_bytes = geo + shb + sort_bytes + 256;
     if (stage_bytes > c->stage_bytes) {
         if (c->stage) cudaFree(c->stage);
         c->stage = nullptr;
@@ -479,13 +501,23 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
         CTX_TRY(c, cudaMalloc(&c->stage, stage_bytes));
         c->stage_bytes = stage_bytes;
     }
-    double* st = static_cast<double*>(c->stage);
+    char* p = static_cast<char*>(c->stage);
+    double* st = reinterpret_cast<double*>(p);                       // means | scales | rots | opacity
+    float4* sh_st = reinterpret_cast<float4*>(p + geo);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(p + geo + shb);
+    uint32_t* keys_alt = keys + n;
+    uint32_t* vals = keys + 2 * n;
+    uint32_t* vals_alt = keys + 3 * n;
+    unsigned long long* bb = reinterpret_cast<unsigned long long*>(keys + 4 * n);
+    void* scratch = reinterpret_cast<char*>(bb) + 64;
     CTX_TRY(c, cudaMemcpyAsync(st, means, sizeof(double) * 3 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(s->dev.opacity, opac, sizeof(double) * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(s->dev.sh4, sh, sizeof(float) * 48 * n, kind, c->stream));
-    launch_deinterleave(st, n, s->dev, c->stream);
+    CTX_TRY(c, cudaMemcpyAsync(st + 10 * n, opac, sizeof(double) * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(sh_st, sh, shb, kind, c->stream));
+    launch_morton_order(st, n, bb, keys, vals, c->stream);
+    const bool alt = radix_sort_u32(keys, keys_alt, vals, vals_alt, nullptr, n, 0, 30, scratch, c->stream, nullptr);
+    launch_gather_scene(st, st + 10 * n, sh_st, alt ? vals_alt : vals, n, s->dev, c->stream);
     CTX_TRY(c, cudaStreamSynchronize(c->stream));
     CTX_TRY(c, cudaGetLastError());
     return PS_OK;
@@ -499,7 +531,8 @@ int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
     const int64_t cap = std::max<int64_t>(n, 1);
     const size_t plane = (sizeof(double) * cap + 255) & ~size_t(255);
     const size_t shb = (sizeof(float) * 48 * cap + 255) & ~size_t(255);
-    cudaError_t e = cudaMalloc(&s->block, 11 * plane + shb);
+    const size_t origb = (sizeof(uint32_t) * cap + 255) & ~size_t(255);
+    cudaError_t e = cudaMalloc(&s->block, 11 * plane + shb + origb);
     if (e != cudaSuccess) {
         delete s;
         return cuda_err(c, e, "cudaMalloc(scene)");
@@ -510,6 +543,8 @@ int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
     for (int k = 0; k < 4; ++k) { s->dev.rot[k] = reinterpret_cast<double*>(p); p += plane; }
     s->dev.opacity = reinterpret_cast<double*>(p); p += plane;
     s->dev.sh4 = reinterpret_cast<float4*>(p);
+    p += shb;
+    s->dev.orig = reinterpret_cast<uint32_t*>(p);
     *out = s;
     return PS_OK;
 }
@@ -601,6 +636,14 @@ int ps_ctx_synchronize(ps_ctx* c) {
 }
 
 void* ps_ctx_stream(ps_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int ps_measure_fp64_peak(ps_ctx* c, double* tflops) {
+    if (!c || !tflops) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    *tflops = measure_fp64_tflops(c->sm_count, c->stream);
+    CTX_TRY(c, cudaGetLastError());
+    return PS_OK;
+}
 
 int ps_measure_fp32_peak(ps_ctx* c, double* tflops) {
     if (!c || !tflops) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
@@ -764,9 +807,20 @@ int ps_prepare(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_conf
     CTX_TRY(c, cudaMemcpy(cov.data(), c->cov_dbg, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
     CTX_TRY(c, cudaMemcpy(b1.data(), f.bl1, sizeof(float4) * n, cudaMemcpyDeviceToHost));
     CTX_TRY(c, cudaMemcpy(b2.data(), f.bl2, sizeof(float2) * n, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> orig(n);
+    CTX_TRY(c, cudaMemcpy(orig.data(), s->dev.orig, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    // the device sort is stable in internal (Morton) order; the reference breaks
+    // depth ties by the original index (raster.cpp:172-175)
+    for (int64_t a = 0; a < v;) {
+        int64_t b = a + 1;
+        while (b < v && kk[b] == kk[a]) ++b;
+        if (b - a > 1)
+            std::sort(idx.begin() + a, idx.begin() + b, [&](uint32_t x, uint32_t y) { return orig[x] < orig[y]; });
+        a = b;
+    }
     for (int64_t k = 0; k < v; ++k) {
         const uint32_t i = idx[k];
-        if (out->index) out->index[k] = i;
+        if (out->index) out->index[k] = orig[i];
         if (out->depth) { double d; std::memcpy(&d, &kk[k], 8); out->depth[k] = d; }
         if (out->mean2d) { out->mean2d[2 * k] = m[i].x; out->mean2d[2 * k + 1] = m[i].y; }
         if (out->conic) { out->conic[3 * k] = ab[i].x; out->conic[3 * k + 1] = ab[i].y; out->conic[3 * k + 2] = cq[i].x; }
@@ -804,9 +858,13 @@ int ps_tile_lists(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_c
         }
         tile_offsets[n_tiles] = static_cast<uint32_t>(r.pairs);
     }
-    if (splat_index && r.pairs)
+    if (splat_index && r.pairs) {
         CTX_TRY(c, cudaMemcpy(splat_index, r.pairs_in_alt ? c->f.pval_alt : c->f.pval,
                               sizeof(uint32_t) * r.pairs, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> orig(s->n);
+        CTX_TRY(c, cudaMemcpy(orig.data(), s->dev.orig, sizeof(uint32_t) * s->n, cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < r.pairs; ++k) splat_index[k] = orig[splat_index[k]];
+    }
     return PS_OK;
 }
 

@@ -81,10 +81,34 @@ __device__ int blend_threshold(const ps_kernel& k, double o, double eps, double&
 // [q* - Gq, q* + Gq] are re-decided in fp64. eT bounds the per-blend relative
 // error of the fp32 transmittance; pixels whose T lands within the accumulated
 // bound of the floor are replayed exactly.
-__device__ void blend_record(double a, double b, double c, double o, double mx, double my,
-                             const FrameParams& P, float cr, float cg, float cb, float4& r0,
-                             float4& r1, float2& r2) {
-    (void)mx; (void)my;
+// Blend kernel classes for K1b: exponential, polynomial of effective order 1..3.
+enum BlendClass : int { kBkExp = 0, kBkP1 = 1, kBkP2 = 2, kBkP3 = 3, kBkGeneric = 4 };
+
+template <int BK>
+__device__ int blend_threshold_t(const ps_kernel& k, double o, double eps, double& qs) {
+    if (BK == kBkGeneric) return blend_threshold(k, o, eps, qs);
+    if (BK == kBkExp) {
+        if (!(o > eps)) return 0;
+        qs = 2.0 * log(o / eps);
+        return 1;
+    }
+    if (!(o * k.coeffs[0] > eps)) return 0;
+    double c[4] = {k.coeffs[0] - eps / o, k.coeffs[1], k.coeffs[2], k.coeffs[3]};
+    if (!(c[0] > 0.0)) return 2;
+    double x = 0.0;
+    int st;
+    if (BK == kBkP1) { st = root_linear(c[0], c[1], x); if (st == PS_OK) x = polish_root(c, 2, x); }
+    else if (BK == kBkP2) { st = root_quadratic(c, x); if (st == PS_OK) x = polish_root(c, 3, x); }
+    else { st = root_cubic(c, x); if (st == PS_OK) x = polish_root(c, 4, x); }
+    if (st != PS_OK) return 2;
+    qs = x;
+    return 1;
+}
+
+
+template <int BK>
+__device__ void blend_record(double a, double b, double c, double o, const FrameParams& P, float cr, float cg,
+                             float cb, float4& r0, float4& r1, float2& r2) {
     const double e32 = 5.9604644775390625e-08; // 2^-24
     const double e64 = 1.1102230246251565e-16; // 2^-53
     const ps_kernel& k = P.cfg.kernel;
@@ -93,7 +117,7 @@ __device__ void blend_record(double a, double b, double c, double o, double mx, 
     double beta = b / a;
     double gamma = c - b * b / a;
     double qs = 0.0;
-    int th = blend_threshold(k, o, eps, qs);
+    int th = blend_threshold_t<BK>(k, o, eps, qs);
     float qhi, qlo, eT;
     bool ok = a > 0.0 && gamma > 0.0 && isfinite(beta) && isfinite(gamma);
     double amax = k.kind == PS_KERNEL_EXPONENTIAL ? o : o * k.coeffs[0];
@@ -161,12 +185,173 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 
 } // namespace
 
+// Tight-tile decision (raster.cpp:103-128) without per-test divisions: the
+// edge minimisers use the per-splat multipliers kx = -b/c, ky = -b/a instead of
+// ((-b)*d)/c. That perturbs the box minimum by at most ~40 ulp of
+// scale = a X^2 + 2|b| X Y + c Y^2 (X, Y = the box's largest |offsets|), so any
+// decision with |m_fast - qroot| > 1e-12 scale equals the reference's; the rest
+// re-run the reference arithmetic exactly.
+struct TightSplat {
+    Sym2 cn;
+    double mx, my, qroot, kx, ky;
+};
+
+__device__ __forceinline__ TightSplat make_tight(const Sym2& cn, double mx, double my, double qroot) {
+    TightSplat t{cn, mx, my, qroot, 0.0, 0.0};
+    t.kx = cn.yy != 0.0 ? -cn.xy / cn.yy : 0.0;
+    t.ky = cn.xx != 0.0 ? -cn.xy / cn.xx : 0.0;
+    return t;
+}
+
+__device__ __forceinline__ bool tight_test_fast(const TightSplat& t, int tx, int ty, int ts) {
+    const double x0 = tx * static_cast<double>(ts) + 0.5;
+    const double y0 = ty * static_cast<double>(ts) + 0.5;
+    const double bx1 = x0 + ts - 1, by1 = y0 + ts - 1;
+    const double lx = x0 - t.mx, hx = bx1 - t.mx;
+    const double ly = y0 - t.my, hy = by1 - t.my;
+    if (lx <= 0.0 && hx >= 0.0 && ly <= 0.0 && hy >= 0.0) return 0.0 <= t.qroot;
+    const Sym2& c = t.cn;
+    double dy = std_clamp(c.yy != 0.0 ? t.kx * lx : ly, ly, hy);
+    double m = quadric(c, lx, dy);
+    dy = std_clamp(c.yy != 0.0 ? t.kx * hx : ly, ly, hy);
+    m = std_min(m, quadric(c, hx, dy));
+    double dx = std_clamp(c.xx != 0.0 ? t.ky * ly : lx, lx, hx);
+    m = std_min(m, quadric(c, dx, ly));
+    dx = std_clamp(c.xx != 0.0 ? t.ky * hy : lx, lx, hx);
+    m = std_min(m, quadric(c, dx, hy));
+    const double X = fmax(fabs(lx), fabs(hx)), Y = fmax(fabs(ly), fabs(hy));
+    const double scale = fabs(c.xx) * X * X + 2.0 * fabs(c.xy) * X * Y + fabs(c.yy) * Y * Y;
+    const double tol = 1e-12 * scale;
+    if (isfinite(m) && isfinite(tol)) {
+        if (m < t.qroot - tol) return true;
+        if (m > t.qroot + tol) return false;
+    }
+    return min_quadric_over_box(c, t.mx, t.my, x0, y0, bx1, by1) <= t.qroot; // exact reference path
+}
+
+// tile_rect (raster.cpp:71-86); for a power-of-two tile size x / ts is an
+// exact scaling, so multiplying by 1/ts gives the same bits as the division.
+__device__ __forceinline__ bool tile_rect_fast(double mx, double my, double cov_xx, double cov_yy, double radius,
+                                               int ts, int width, int height, int r[4]) {
+    if (ts & (ts - 1)) return tile_rect(mx, my, cov_xx, cov_yy, radius, ts, width, height, r);
+    const double inv = 1.0 / ts;
+    const double hx = radius * sqrt(std_max(cov_xx, 0.0));
+    const double hy = radius * sqrt(std_max(cov_yy, 0.0));
+    const int tiles_x = (width + ts - 1) / ts;
+    const int tiles_y = (height + ts - 1) / ts;
+    int x0 = x86_cvtt_int(floor((mx - hx) * inv));
+    int x1 = x86_cvtt_int(floor((mx + hx) * inv));
+    int y0 = x86_cvtt_int(floor((my - hy) * inv));
+    int y1 = x86_cvtt_int(floor((my + hy) * inv));
+    x0 = imax(x0, 0);
+    y0 = imax(y0, 0);
+    x1 = imin(x1, tiles_x - 1);
+    y1 = imin(y1, tiles_y - 1);
+    if (x0 > x1 || y0 > y1) return false;
+    r[0] = x0; r[1] = y0; r[2] = x1; r[3] = y1;
+    return true;
+}
+
+// Block-level tile aggregation. Splats are Morton-ordered, so one CTA's splats
+// cover a compact screen region: per-tile counts / bucket slots are gathered
+// in a shared-memory window over the union of the CTA's tile rects, and only
+// one global atomic per distinct tile per CTA is issued. Rects of > 64 tiles
+// (or a window larger than kWinCap) fall back to direct global atomics.
+constexpr int kWinCap = 1024;
+
+struct Window {
+    int x0, y0, w, h;
+    bool ok;
+};
+
+__device__ __forceinline__ Window block_window(bool has, const int r[4], int* wb) {
+    if (threadIdx.x == 0) { wb[0] = INT_MAX; wb[1] = INT_MAX; wb[2] = -1; wb[3] = -1; }
+    __syncthreads();
+    if (has) {
+        atomicMin(&wb[0], r[0]);
+        atomicMin(&wb[1], r[1]);
+        atomicMax(&wb[2], r[2]);
+        atomicMax(&wb[3], r[3]);
+    }
+    __syncthreads();
+    Window w;
+    w.x0 = wb[0];
+    w.y0 = wb[1];
+    w.w = wb[2] - wb[0] + 1;
+    w.h = wb[3] - wb[1] + 1;
+    w.ok = wb[2] >= 0 && w.w * w.h <= kWinCap;
+    return w;
+}
+
+__device__ __forceinline__ int rect_bit_tile(const int r[4], int b, int tiles_x) {
+    const int w = r[2] - r[0] + 1;
+    return (r[1] + b / w) * tiles_x + r[0] + b % w;
+}
+
+__device__ __forceinline__ int rect_bit_win(const int r[4], int b, const Window& W) {
+    const int w = r[2] - r[0] + 1;
+    return (r[1] + b / w - W.y0) * W.w + (r[0] + b % w - W.x0);
+}
+
 // ------------------------------------------------------------ K1 preprocess
-__global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, FrameDev f,
-                                                    DevCounters* ctr) {
+// Split in two so each variant stays small (the all-modes kernel thrashed the
+// instruction cache):
+//   K1a k_geometry<BC>: project_splat (projection.cpp:36-79), culling_bound_for
+//       specialised on the culling class (raster.cpp:50-69, kernel.cpp:335-369),
+//       tile_rect (raster.cpp:71-86) and the tight-tile bitmask (raster.cpp:126-128).
+//   K1b k_shade<BK>: SH colour (projection.cpp:93-116) + the fp32 blend record,
+//       specialised on the blend kernel.
+enum BoundClass : int { kBcStp = 0, kBcZero = 1, kBcOaExp = 2, kBcOaP1 = 3, kBcOaP2 = 4, kBcOaP3 = 5, kBcGeneric = 6 };
+
+// culling_bound_for specialised per class. 1 = bound set, 0 = nullopt (below
+// epsilon, uncounted), -status on error. Same arithmetic as exact_math.cuh.
+template <int BC>
+__device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double& radius, double& qroot) {
+    if (BC == kBcGeneric) return culling_bound_for(cfg, o, radius, qroot);
+    if (!(o > 0.0)) return 0;
+    double x = 0.0;
+    if (BC == kBcStp) {
+        if (!(o > cfg.epsilon)) return 0;
+        x = 2.0 * log(o / cfg.epsilon);
+    } else if (BC == kBcZero) {
+        x = (cfg.has_culling_kernel ? cfg.culling_kernel : cfg.kernel).first_root;
+    } else {
+        const ps_kernel& k = cfg.has_culling_kernel ? cfg.culling_kernel : cfg.kernel;
+        if (o > 1.0) return -PS_INVALID_ARGUMENT; // culling_radius: opacity must be in (0,1]
+        if (BC == kBcOaExp) {
+            if (!(o > cfg.epsilon)) return 0;
+            x = 2.0 * log(o / cfg.epsilon);
+        } else {
+            if (!(o * k.coeffs[0] > cfg.epsilon)) return 0;
+            double c[4] = {k.coeffs[0] - cfg.epsilon / o, k.coeffs[1], k.coeffs[2], k.coeffs[3]};
+            if (!(c[0] > 0.0)) return -PS_INVALID_ARGUMENT;
+            int st;
+            if (BC == kBcOaP1) {
+                st = root_linear(c[0], c[1], x);
+                if (st == PS_OK) x = polish_root(c, 2, x);
+            } else if (BC == kBcOaP2) {
+                st = root_quadratic(c, x);
+                if (st == PS_OK) x = polish_root(c, 3, x);
+            } else {
+                st = root_cubic(c, x);
+                if (st == PS_OK) x = polish_root(c, 4, x);
+            }
+            if (st != PS_OK) return -st;
+        }
+    }
+    qroot = x + kBoundSlack;
+    radius = sqrt(qroot);
+    return 1;
+}
+
+template <int BC>
+__global__ void __launch_bounds__(256) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
+    bool small = false;
+    unsigned long long my_mask = 0ull;
+    int my_r[4] = {0, 0, -1, -1};
     if (i < s.n) {
         unsigned long long key = ~0ull;
         uint32_t cnt = 0;
@@ -175,21 +360,20 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
         const double quat[4] = {s.rot[0][i], s.rot[1][i], s.rot[2][i], s.rot[3][i]};
         const double opacity = s.opacity[i];
         Projected pr;
-        int st = project(mean, scale, quat, opacity, P.cam, P.cfg.v_dilation, pr);
+        const int st = project(mean, scale, quat, opacity, P.cam, P.cfg.v_dilation, pr);
         if (st < 0) {
             raise_error(ctr, -st, i);
         } else if (st == 0) {
             frustum = 1; // kFrustum (raster.cpp:144-146,162-163)
         } else {
             double radius = 0.0, qroot = 0.0;
-            int b = culling_bound_for(P.cfg, pr.opacity_eff, radius, qroot);
+            const int b = bound_for<BC>(P.cfg, pr.opacity_eff, radius, qroot);
             if (b < 0) {
                 raise_error(ctr, -b, i);
             } else if (b > 0) { // b == 0: below epsilon, dropped uncounted (raster.cpp:149-151)
                 int r[4];
                 const int ts = P.cfg.tile_size;
-                if (!tile_rect(pr.mx, pr.my, pr.cov_aa.xx, pr.cov_aa.yy, radius, ts, P.cam.width,
-                               P.cam.height, r)) {
+                if (!tile_rect_fast(pr.mx, pr.my, pr.cov_aa.xx, pr.cov_aa.yy, radius, ts, P.cam.width, P.cam.height, r)) {
                     frustum = 1; // off screen (raster.cpp:165-168)
                 } else {
                     visible = 1;
@@ -197,17 +381,23 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
                              static_cast<unsigned long long>(r[3] - r[1] + 1);
                     unsigned long long mask = 0ull;
                     int bit = 0;
+                    const bool big = coarse > 64;
+                    const TightSplat tsp = make_tight(pr.conic, pr.mx, pr.my, qroot);
                     for (int ty = r[1]; ty <= r[3]; ++ty)
                         for (int tx = r[0]; tx <= r[2]; ++tx, ++bit)
-                            if (tight_tile_test(pr.conic, pr.mx, pr.my, qroot, tx, ty, ts)) {
+                            if (tight_test_fast(tsp, tx, ty, ts)) {
                                 ++cnt;
-                                if (bit < 64) mask |= 1ull << bit;
+                                if (!big) mask |= 1ull << bit;
+                                else if (f.tile_count) atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u);
                             }
-                    f.tmask[i] = mask;
+                    small = !big && cnt > 0;
+                    my_mask = mask;
+                    for (int k = 0; k < 4; ++k) my_r[k] = r[k];
                     tight = cnt;
                     key = static_cast<unsigned long long>(__double_as_longlong(pr.depth));
                     kmin_inv = ~key;
                     kmax = key;
+                    f.tmask[i] = mask;
                     f.mean2d[i] = make_double2(pr.mx, pr.my);
                     f.conic_ab[i] = make_double2(pr.conic.xx, pr.conic.xy);
                     f.conic_cq[i] = make_double2(pr.conic.yy, qroot);
@@ -219,28 +409,6 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
                         f.cov_aa[3 * i + 1] = pr.cov_aa.xy;
                         f.cov_aa[3 * i + 2] = pr.cov_aa.yy;
                     }
-                    float v[48];
-#pragma unroll
-                    for (int j = 0; j < kShPlanes; ++j) {
-                        float4 t = j < P.sh_floats4 ? s.sh4[i * kShPlanes + j]
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
-                    }
-                    float col[3];
-                    sh_color(v, P.cfg.sh_degree, static_cast<float>(pr.dir[0]),
-                             static_cast<float>(pr.dir[1]), static_cast<float>(pr.dir[2]), col);
-                    if (P.cfg.clamp_before_blend) {
-                        col[0] = fminf(fmaxf(col[0], 0.f), 1.f);
-                        col[1] = fminf(fmaxf(col[1], 0.f), 1.f);
-                        col[2] = fminf(fmaxf(col[2], 0.f), 1.f);
-                    }
-                    float4 r0, r1;
-                    float2 r2;
-                    blend_record(pr.conic.xx, pr.conic.xy, pr.conic.yy, pr.opacity_eff, pr.mx, pr.my, P,
-                                 col[0], col[1], col[2], r0, r1, r2);
-                    f.bl0[i] = r0;
-                    f.bl1[i] = r1;
-                    f.bl2[i] = r2;
                 }
             }
         }
@@ -248,25 +416,86 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneDev s, FrameParams P, F
         f.val[i] = static_cast<uint32_t>(i);
         f.tcount[i] = cnt;
     }
+    if (f.tile_count) { // tight pairs per tile for the bucket scan (K2)
+        __shared__ uint32_t win[kWinCap];
+        __shared__ int wb[4];
+        const Window W = block_window(small, my_r, wb);
+        if (W.ok) {
+            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) win[k] = 0;
+            __syncthreads();
+            if (small) {
+                unsigned long long m = my_mask;
+                while (m) {
+                    const int b = __ffsll(static_cast<long long>(m)) - 1;
+                    m &= m - 1;
+                    atomicAdd(&win[rect_bit_win(my_r, b, W)], 1u);
+                }
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x)
+                if (win[k]) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], win[k]);
+        } else if (small) {
+            unsigned long long m = my_mask;
+            while (m) {
+                const int b = __ffsll(static_cast<long long>(m)) - 1;
+                m &= m - 1;
+                atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
+            }
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kmin_inv = max(kmin_inv, __shfl_xor_sync(0xffffffffu, kmin_inv, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if ((threadIdx.x & 31) == 0 && kmax) {
-        atomicMax(&ctr->key_min, kmin_inv);
-        atomicMax(&ctr->key_max, kmax);
     }
     frustum = warp_sum_u64(frustum);
     coarse = warp_sum_u64(coarse);
     tight = warp_sum_u64(tight);
     visible = warp_sum_u64(visible);
     if ((threadIdx.x & 31) == 0) {
+        if (kmax) {
+            atomicMax(&ctr->key_min, kmin_inv);
+            atomicMax(&ctr->key_max, kmax);
+        }
         if (frustum) atomicAdd(&ctr->frustum, frustum);
         if (coarse) atomicAdd(&ctr->coarse, coarse);
         if (tight) atomicAdd(&ctr->tight, tight);
         if (visible) atomicAdd(&ctr->visible, visible);
     }
+}
+
+template <int BK>
+__global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameDev f, double3 campos) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s.n || f.key[i] == ~0ull) return;
+    // view direction (mean - camera position), normalised; fp32 suffices for colour
+    const float dx = static_cast<float>(s.mean[0][i] - campos.x);
+    const float dy = static_cast<float>(s.mean[1][i] - campos.y);
+    const float dz = static_cast<float>(s.mean[2][i] - campos.z);
+    const float nrm = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
+    float v[48];
+#pragma unroll
+    for (int j = 0; j < kShPlanes; ++j) {
+        const float4 t = j < P.sh_floats4 ? s.sh4[i * kShPlanes + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
+    }
+    float col[3];
+    sh_color(v, P.cfg.sh_degree, dx * inv, dy * inv, dz * inv, col);
+    if (P.cfg.clamp_before_blend) {
+        col[0] = fminf(fmaxf(col[0], 0.f), 1.f);
+        col[1] = fminf(fmaxf(col[1], 0.f), 1.f);
+        col[2] = fminf(fmaxf(col[2], 0.f), 1.f);
+    }
+    const double2 ab = f.conic_ab[i];
+    const double2 cq = f.conic_cq[i];
+    float4 r0, r1;
+    float2 r2;
+    blend_record<BK>(ab.x, ab.y, cq.x, f.opacity_eff[i], P, col[0], col[1], col[2], r0, r1, r2);
+    f.bl0[i] = r0;
+    f.bl1[i] = r1;
+    f.bl2[i] = r2;
+    (void)0;
 }
 
 // ------------------------------------------------------------ K3 duplicate
@@ -316,30 +545,71 @@ __device__ __forceinline__ void for_each_tight_tile(const FrameDev& f, const Fra
     const double2 mm = f.mean2d[i];
     const double2 ab = f.conic_ab[i];
     const double2 cq = f.conic_cq[i];
-    const Sym2 cn{ab.x, ab.y, cq.x};
+    const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
     const int ts = P.cfg.tile_size;
     for (int ty = rc.y; ty <= rc.w; ++ty)
         for (int tx = rc.x; tx <= rc.z; ++tx)
-            if (tight_tile_test(cn, mm.x, mm.y, cq.y, tx, ty, ts)) fn(ty * P.tiles_x + tx);
+            if (tight_test_fast(t, tx, ty, ts)) fn(ty * P.tiles_x + tx);
 }
 
-// K1c: pairs per tile (red.add; result unused).
-__global__ void __launch_bounds__(256) k_count_tiles(FrameDev f, FrameParams P, int64_t n) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n || f.tcount[i] == 0) return;
-    for_each_tight_tile(f, P, i, [&](int t) { atomicAdd(&f.tile_count[t * kCounterStride], 1u); });
-}
-
-// K3 (bucketed): splat indices into per-tile buckets at atomically claimed
-// slots. The order inside a bucket is arbitrary; K4 sorts each bucket by the
-// reference's exact key.
+// K3 (bucketed): splat indices into per-tile buckets. A CTA counts its pairs
+// per tile in the shared window, reserves one contiguous slot range per
+// distinct tile with a single global atomic, then hands out slots with shared
+// atomics. Bucket order is arbitrary; K4 sorts each bucket by the reference's
+// exact key.
 __global__ void __launch_bounds__(256) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
+    __shared__ uint32_t win[kWinCap];
+    __shared__ int wb[4];
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n || f.tcount[i] == 0) return;
-    for_each_tight_tile(f, P, i, [&](int t) {
-        const uint32_t slot = atomicAdd(&f.tile_count[t * kCounterStride], 1u);
-        f.pval[slot] = static_cast<uint32_t>(i);
-    });
+    const bool active = i < n && f.tcount[i] != 0;
+    int r[4] = {0, 0, -1, -1};
+    unsigned long long m0 = 0ull;
+    bool small = false;
+    if (active) {
+        const ushort4 rc = f.rect[i];
+        r[0] = rc.x; r[1] = rc.y; r[2] = rc.z; r[3] = rc.w;
+        if ((r[2] - r[0] + 1) * (r[3] - r[1] + 1) <= 64) {
+            small = true;
+            m0 = f.tmask[i];
+        } else { // big rect: exact tests, direct atomics (rare)
+            const double2 mm = f.mean2d[i];
+            const double2 ab = f.conic_ab[i];
+            const double2 cq = f.conic_cq[i];
+            const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
+            for (int ty = r[1]; ty <= r[3]; ++ty)
+                for (int tx = r[0]; tx <= r[2]; ++tx)
+                    if (tight_test_fast(t, tx, ty, P.cfg.tile_size))
+                        f.pval[atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u)] = static_cast<uint32_t>(i);
+        }
+    }
+    const Window W = block_window(small, r, wb);
+    if (W.ok) {
+        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) win[k] = 0;
+        __syncthreads();
+        unsigned long long m = m0;
+        while (m) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            atomicAdd(&win[rect_bit_win(r, b, W)], 1u);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x)
+            if (win[k]) win[k] = atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], win[k]);
+        __syncthreads();
+        m = m0;
+        while (m) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            f.pval[atomicAdd(&win[rect_bit_win(r, b, W)], 1u)] = static_cast<uint32_t>(i);
+        }
+    } else if (small) {
+        unsigned long long m = m0;
+        while (m) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            f.pval[atomicAdd(&f.tile_count[rect_bit_tile(r, b, P.tiles_x)], 1u)] = static_cast<uint32_t>(i);
+        }
+    }
 }
 
 // ------------------------------------------------------------ K7 exact replay
@@ -432,7 +702,23 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
                        cudaStream_t st) {
     if (s.n == 0) return;
     const int blocks = static_cast<int>((s.n + 255) / 256);
-    k_preprocess<<<blocks, 256, 0, st>>>(s, P, f, ctr);
+    switch (P.bound_class) {
+        case kBcStp: k_geometry<kBcStp><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        case kBcZero: k_geometry<kBcZero><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        case kBcOaExp: k_geometry<kBcOaExp><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        case kBcOaP1: k_geometry<kBcOaP1><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        case kBcOaP2: k_geometry<kBcOaP2><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        case kBcOaP3: k_geometry<kBcOaP3><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+        default: k_geometry<kBcGeneric><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
+    }
+    const double3 cp = make_double3(P.campos[0], P.campos[1], P.campos[2]);
+    switch (P.blend_class) {
+        case kBkExp: k_shade<kBkExp><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+        case kBkP1: k_shade<kBkP1><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+        case kBkP2: k_shade<kBkP2><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+        case kBkP3: k_shade<kBkP3><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+        default: k_shade<kBkGeneric><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+    }
 }
 
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
@@ -440,12 +726,6 @@ void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* o
     if (n == 0) return;
     const int blocks = static_cast<int>((n + 255) / 256);
     k_duplicate<<<blocks, 256, 0, st>>>(f, P, order, n);
-}
-
-void launch_count_tiles(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st) {
-    if (n == 0) return;
-    const int blocks = static_cast<int>((n + 255) / 256);
-    k_count_tiles<<<blocks, 256, 0, st>>>(f, P, n);
 }
 
 void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st) {

@@ -95,11 +95,11 @@ struct Projected {
     double mx, my;
     Sym2 conic, cov_aa;
     double depth, opacity_eff;
-    double dir[3]; // normalized view direction (mean - camera position)
 };
 
-// projection.cpp:36-79 project_splat. Returns 1 visible, 0 behind the near
-// plane, -PS_DEGENERATE_COVARIANCE when det(cov_aa) <= 1e-12.
+// projection.cpp:36-79 project_splat (geometry part; the SH colour of :77 is
+// evaluated separately in fp32). Returns 1 visible, 0 behind the near plane,
+// -PS_DEGENERATE_COVARIANCE when det(cov_aa) <= 1e-12.
 PS_HD int project(const double mean[3], const double scale[3], const double quat[4], double opacity,
                   const ps_camera& cam, double v, Projected& out) {
     const double* R = cam.rotation;
@@ -142,14 +142,6 @@ PS_HD int project(const double mean[3], const double scale[3], const double quat
     out.conic = inverse(cov_aa);
     out.depth = pz;
     out.opacity_eff = opacity * ratio;
-    // Camera::position (projection.hpp:29 / geometry.hpp:90-94), Vec3::normalized (:22-26)
-    double cpx = (R[0] * t[0] + R[3] * t[1] + R[6] * t[2]) * -1.0;
-    double cpy = (R[1] * t[0] + R[4] * t[1] + R[7] * t[2]) * -1.0;
-    double cpz = (R[2] * t[0] + R[5] * t[1] + R[8] * t[2]) * -1.0;
-    double dx = mean[0] - cpx, dy = mean[1] - cpy, dz = mean[2] - cpz;
-    double n = sqrt(dx * dx + dy * dy + dz * dz);
-    if (n > 0.0) { out.dir[0] = dx / n; out.dir[1] = dy / n; out.dir[2] = dz / n; }
-    else { out.dir[0] = 0.0; out.dir[1] = 0.0; out.dir[2] = 0.0; }
     return 1;
 }
 

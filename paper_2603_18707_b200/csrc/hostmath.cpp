@@ -28,6 +28,23 @@ namespace ps {
 extern thread_local std::string g_free_error;
 
 int host_validate_config(const ps_config& c) { return validate_config(c); }
+
+// first_positive_root's degenerate-leading-coefficient trim (kernel.cpp:124):
+// the coefficient count the root solver actually uses.
+int host_effective_terms(const ps_kernel& k) {
+    int n = k.order + 1;
+    while (n > 1 && std::fabs(k.coeffs[n - 1]) < 1e-12) --n;
+    return n;
+}
+
+// Camera::position() = R^T t * -1 (projection.hpp:29, geometry.hpp:90-94).
+void host_camera_position(const ps_camera& cam, double out[3]) {
+    const double* R = cam.rotation;
+    const double* t = cam.translation;
+    out[0] = (R[0] * t[0] + R[3] * t[1] + R[6] * t[2]) * -1.0;
+    out[1] = (R[1] * t[0] + R[4] * t[1] + R[7] * t[2]) * -1.0;
+    out[2] = (R[2] * t[0] + R[5] * t[1] + R[8] * t[2]) * -1.0;
+}
 int host_validate_camera(const ps_camera& c) { return validate_camera(c); }
 
 // Blend-threshold mode (see blend.cu): the quadric-space skip test is exact iff

@@ -13,7 +13,6 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
                        cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
                       cudaStream_t st);
-void launch_count_tiles(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
 void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
                    float* out_t, bool count_work, int sm_count, cudaStream_t st);
@@ -46,8 +45,8 @@ void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCount
                       cudaStream_t st);
 // sorts every bucket with 1 < length <= max_items (shared memory); returns false
 // when max_items exceeds what one CTA can hold (caller falls back)
-bool launch_tile_sort(const FrameDev& f, int n_tiles, uint32_t max_len, const DevCounters* d_ctr, cudaStream_t st,
-                      int* launches);
+bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint32_t max_len,
+                      const DevCounters* d_ctr, cudaStream_t st, int* launches);
 
 // blend.cu (K6)
 struct BlendOut {
@@ -59,6 +58,12 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
 
 // utils.cu
 void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st);
+// scene reordering along a 30-bit Morton curve of the means (upload time)
+void launch_morton_order(const double* means, int64_t n, unsigned long long* bb, uint32_t* keys, uint32_t* vals,
+                         cudaStream_t st);
+void launch_gather_scene(const double* staging, const double* opac, const float4* sh, const uint32_t* perm,
+                         int64_t n, const SceneDev& s, cudaStream_t st);
 double measure_fp32_tflops(int sm_count, cudaStream_t st);
+double measure_fp64_tflops(int sm_count, cudaStream_t st);
 
 } // namespace ps

@@ -10,7 +10,7 @@ ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 frames, cur = [], []
 for r in rows[hi + 1:]:
     name = re.sub(r"\(.*", "", r[ki])
-    if "k_preprocess" in name and cur:
+    if ("k_preprocess" in name or "k_geometry" in name) and cur:
         frames.append(cur)
         cur = []
     cur.append((name[-50:], float(r[vi].replace(",", ""))))
