@@ -11,6 +11,7 @@
 //      splat index) — a total order, so the arbitrary scatter order of K3 does
 //      not matter and the result equals the reference's per-tile list.
 #include "kernels.h"
+#include "tile_sort.cuh"
 
 namespace ps {
 
@@ -67,213 +68,6 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
     }
 }
 
-// Exact per-tile order (the reference comparator, raster.cpp:172-175:
-// fp64 depth, then splat index; positive fp64 depths order like their bits):
-//  1. 16-bit key = top bits of (depth bits - tile minimum) over the tile's own
-//     depth span; stable LSD radix sort, 2 x 8-bit digits. Stable ranking: each
-//     warp owns a contiguous slice of the current order and ranks it 32 items
-//     at a time with match.any.
-//  2. every run of equal 16-bit keys is re-ordered by the full (bits, index)
-//     key; runs are expected to be ~L^2/2^17 pairs, so a thread insertion-sorts
-//     each. A run longer than kMaxRun (degenerate depth clusters) switches the
-//     CTA to a bitonic sort on the full key, which is exact for any input.
-constexpr int kMaxRun = 64;
-
-template <int THREADS, int ROUNDS>
-struct TileSortSmem {
-    static constexpr int CAP = THREADS * ROUNDS;
-    static constexpr int WARPS = THREADS / 32;
-    static constexpr size_t bytes() {
-        // keys16 x2 (as u32), vals x2, full keys, per-warp digit counts
-        return sizeof(uint32_t) * (4 * CAP + WARPS * 256) + sizeof(unsigned long long) * CAP;
-    }
-};
-
-template <int THREADS, int ROUNDS>
-__device__ void sort_one_tile(const uint2 r, uint32_t* __restrict__ pval, const unsigned long long* __restrict__ key,
-                              const uint32_t* __restrict__ orig, uint32_t* smem) {
-    constexpr int WARPS = THREADS / 32;
-    constexpr int CAP = THREADS * ROUNDS;
-    uint32_t* kbuf = smem;                                     // [2][CAP]
-    uint32_t* vbuf = smem + 2 * CAP;                           // [2][CAP]
-    uint32_t* whist = smem + 4 * CAP;                          // [WARPS][256]
-    unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem + 4 * CAP + WARPS * 256); // [CAP]
-    __shared__ uint32_t dtot[256];
-    __shared__ uint32_t wsum[WARPS];
-    __shared__ unsigned long long red_min[WARPS], red_max[WARPS];
-    __shared__ int need_bitonic;
-
-    const int L = static_cast<int>(r.y - r.x);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long lo = ~0ull, hi = 0ull;
-    for (int j = threadIdx.x; j < L; j += THREADS) {
-        const uint32_t v = pval[r.x + j];
-        const unsigned long long k = key[v];
-        vbuf[j] = v;
-        fk[j] = k;
-        lo = min(lo, k);
-        hi = max(hi, k);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) { red_min[warp] = lo; red_max[warp] = hi; }
-    if (threadIdx.x == 0) need_bitonic = 0;
-    __syncthreads();
-    lo = red_min[0]; hi = red_max[0];
-    for (int w = 1; w < WARPS; ++w) { lo = min(lo, red_min[w]); hi = max(hi, red_max[w]); }
-    const unsigned long long span = hi - lo;
-    const int shift = span ? max(0, 64 - __clzll(static_cast<long long>(span)) - 16) : 0;
-    for (int j = threadIdx.x; j < L; j += THREADS) kbuf[j] = static_cast<uint32_t>((fk[j] - lo) >> shift);
-    const int per_warp = ((L + WARPS * 32 - 1) / (WARPS * 32)) * 32;
-    uint32_t lt;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    int cur = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int sh = pass * 8;
-        for (int d = threadIdx.x; d < WARPS * 256; d += THREADS) whist[d] = 0;
-        __syncthreads();
-        const uint32_t* kin = kbuf + cur * CAP;
-        const uint32_t* vin = vbuf + cur * CAP;
-        uint32_t* kout = kbuf + (cur ^ 1) * CAP;
-        uint32_t* vout = vbuf + (cur ^ 1) * CAP;
-        uint32_t pos[ROUNDS], dig[ROUNDS], kk[ROUNDS], vv[ROUNDS];
-#pragma unroll
-        for (int it = 0; it < ROUNDS; ++it) {
-            const int j = warp * per_warp + it * 32 + lane;
-            const bool valid = (it * 32 < per_warp) && j < L;
-            kk[it] = valid ? kin[j] : 0u;
-            vv[it] = valid ? vin[j] : 0u;
-            const uint32_t d = valid ? (kk[it] >> sh) & 0xFFu : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t cb = valid ? whist[warp * 256 + d] : 0u;
-            __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) whist[warp * 256 + d] = cb + __popc(peers);
-            __syncwarp();
-            pos[it] = cb + __popc(peers & lt);
-            dig[it] = d;
-        }
-        __syncthreads();
-        for (int d = threadIdx.x; d < 256; d += THREADS) {
-            uint32_t acc = 0;
-            for (int w = 0; w < WARPS; ++w) {
-                const uint32_t c = whist[w * 256 + d];
-                whist[w * 256 + d] = acc;
-                acc += c;
-            }
-            dtot[d] = acc;
-        }
-        __syncthreads();
-        // exclusive scan of the 256 digit totals
-        constexpr int PER = 256 / THREADS > 0 ? 256 / THREADS : 1;
-        if (threadIdx.x * PER < 256) {
-            uint32_t loc[PER];
-            uint32_t sum = 0;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) { loc[q] = dtot[threadIdx.x * PER + q]; sum += loc[q]; }
-            uint32_t x = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) wsum[warp] = x;
-            __syncwarp();
-        }
-        __syncthreads();
-        if (threadIdx.x * PER < 256) {
-            uint32_t woff = 0;
-            for (int w = 0; w < warp; ++w) woff += wsum[w];
-            // recompute this thread's inclusive prefix within the warp
-            uint32_t sum = 0;
-            uint32_t loc[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) { loc[q] = dtot[threadIdx.x * PER + q]; sum += loc[q]; }
-            uint32_t x = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            uint32_t base = woff + x - sum;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int d = threadIdx.x * PER + q;
-                for (int w = 0; w < WARPS; ++w) whist[w * 256 + d] += base;
-                base += loc[q];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < ROUNDS; ++it) {
-            if (dig[it] < 256u) {
-                const uint32_t dst = whist[warp * 256 + dig[it]] + pos[it];
-                kout[dst] = kk[it];
-                vout[dst] = vv[it];
-            }
-        }
-        __syncthreads();
-        cur ^= 1;
-    }
-    const uint32_t* ks = kbuf + cur * CAP;
-    uint32_t* vs = vbuf + cur * CAP;
-    // full keys in the sorted order (the fk array is indexed by original slot)
-    // -> re-gather through the value's global key
-    for (int j = threadIdx.x; j < L; j += THREADS) {
-        if ((j == 0 || ks[j - 1] != ks[j]) && j + 1 < L && ks[j + 1] == ks[j]) {
-            int e = j + 1;
-            while (e < L && ks[e] == ks[j] && e - j <= kMaxRun) ++e;
-            if (e - j > kMaxRun) {
-                need_bitonic = 1;
-                continue;
-            }
-            for (int a = j + 1; a < e; ++a) {
-                const uint32_t va = vs[a];
-                const unsigned long long ka = key[va];
-                int b = a - 1;
-                while (b >= j) {
-                    const uint32_t vb = vs[b];
-                    const unsigned long long kb = key[vb];
-                    if (kb < ka || (kb == ka && orig[vb] < orig[va])) break;
-                    vs[b + 1] = vb;
-                    --b;
-                }
-                vs[b + 1] = va;
-            }
-        }
-    }
-    __syncthreads();
-    if (need_bitonic) {
-        // degenerate depth clusters: exact bitonic sort on (bits, index)
-        int n = 1;
-        while (n < L) n <<= 1;
-        uint32_t* bv = vbuf + (cur ^ 1) * CAP; // free buffer (CAP >= n is not guaranteed: use fk + vs in place)
-        (void)bv;
-        for (int j = threadIdx.x; j < CAP; j += THREADS) {
-            if (j < L) fk[j] = key[vs[j]];
-            else if (j < n) { fk[j] = ~0ull; vs[j] = 0xffffffffu; }
-        }
-        __syncthreads();
-        for (int k = 2; k <= n; k <<= 1)
-            for (int jj = k >> 1; jj > 0; jj >>= 1) {
-                const int lg = __ffs(jj) - 1;
-                for (int p = threadIdx.x; p < (n >> 1); p += THREADS) {
-                    const int i = ((p >> lg) << (lg + 1)) + (p & (jj - 1));
-                    const int ix = i + jj;
-                    const unsigned long long ka = fk[i], kb = fk[ix];
-                    const uint32_t va = vs[i], vb = vs[ix];
-                    const bool gt = ka > kb || (ka == kb && (va == 0xffffffffu ? 0xffffffffu : orig[va]) >
-                                                                   (vb == 0xffffffffu ? 0xffffffffu : orig[vb]));
-                    if (gt == ((i & k) == 0)) { fk[i] = kb; fk[ix] = ka; vs[i] = vb; vs[ix] = va; }
-                }
-                __syncthreads();
-            }
-    }
-    for (int j = threadIdx.x; j < L; j += THREADS) pval[r.x + j] = vs[j];
-}
-
 // Small buckets (length <= CAP): one CTA per tile over the whole grid.
 template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_small(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
@@ -328,6 +122,25 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
                                                                    &d_ctr->big_tiles, 1024);
         if (launches) *launches += 1;
     }
+    if (max_len > 4096u) {
+        using S3 = TileSortSmem<1024, 16>;
+        cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
+        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+                                                                   &d_ctr->big_tiles, 4096);
+        if (launches) *launches += 1;
+    }
+    return true;
+}
+
+bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
+                           cudaStream_t st, int* launches) {
+    if (max_len <= 1024u) return true;
+    if (max_len > 16384u) return false;
+    using S2 = TileSortSmem<512, 8>;
+    cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
+    k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+                                                               &d_ctr->big_tiles, 1024);
+    if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 16>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));

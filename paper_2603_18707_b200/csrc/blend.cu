@@ -12,11 +12,12 @@
 // <=> q <= q*(o). No MUFU on the skip path for any kernel; polynomial kernels
 // evaluate alpha with FFMA only. q in [q_lo, q_hi] (the certified fp32 error
 // band) is re-decided with the reference's fp64 arithmetic (exact_alpha_ge_eps).
-// The transmittance test (raster.cpp:272-277) carries a per-pixel relative
-// error bound eT; a pixel whose T lands inside the band around the floor is
-// flagged and replayed exactly in fp64 by K7. Early termination: the CTA stops
+// The transmittance test (raster.cpp:272-277) carries a per-pixel absolute
+// error bound on T; a pixel whose test value lands inside that band around the
+// floor is flagged and replayed exactly in fp64 by K7. Early termination: the CTA stops
 // when no pixel is live (__syncthreads_count), the reference's `remaining == 0`.
 #include "kernels.h"
+#include "tile_sort.cuh"
 
 namespace ps {
 
@@ -26,6 +27,9 @@ struct BlendArgs {
     FrameParams P;
     const uint2* ranges;
     const uint32_t* pval;
+    uint32_t* pval_w;                  // buckets to sort in the prologue (null: presorted)
+    const unsigned long long* key;     // fp64 depth bits (sort key)
+    const uint32_t* orig;              // original splat index (tie-break)
     const double2* mean2d;
     const float4* bl0;
     const float4* bl1;
@@ -166,14 +170,17 @@ __global__ void k_blend(const BlendArgs A) {
                     }
                 }
                 const float4 v2 = s2[k];
-                eT += v2.x;
-                const float test_t = fmaf(-T, alpha, T);
-                if (test_t < fmaf(floor_f, eT, floor_f)) {
+                // absolute error bound of the fp32 transmittance (see blend_px)
+                const float om = 1.0f - alpha;
+                const float test_t = T * om;
+                const float en = fmaf(2.5f * 5.9604645e-08f, test_t, fmaf(eT, om, T * v2.x));
+                if (test_t < floor_f + en) {
                     done = true;
-                    if (test_t < fmaf(-floor_f, eT, floor_f)) term = static_cast<uint32_t>(base + k);
+                    if (test_t < floor_f - en) term = static_cast<uint32_t>(base + k);
                     else flagged = true;
                     break;
                 }
+                eT = en;
                 const float w = alpha * T;
                 cr = fmaf(v2.y, w, cr);
                 cg = fmaf(v2.z, w, cg);
@@ -234,7 +241,7 @@ struct Px {
 };
 
 // Shared-memory record of one staged splat (tile-local, fp32):
-//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, K0}  c = {eT, r, g, b}
+//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, K0}  c = {g_alpha, r, g, b}
 //   d = {K1, K2, K3, splat index bits}   box = {x_lo, x_hi, y_lo, y_hi}
 // K_j = o c_j folds the opacity into the polynomial (K0 = log2 o for exp);
 // box is the axis-aligned extent of {q <= q_hi} (+ margin) used for warp culling.
@@ -273,11 +280,18 @@ __device__ __forceinline__ void blend_px(Px& p, float q, const float4& sb, const
                 return;
         }
     }
-    p.eT += sc.x;
-    const float test_t = fmaf(-p.T, alpha, p.T);
+    // Transmittance decision (raster.cpp:272-277) with a running ABSOLUTE error
+    // bound e >= |T_fp32 - T_ref|: with g = the splat's |alpha_fp32 - alpha_ref|
+    // bound (sc.x), e' = e (1 - alpha) + T g + 2.5u T' covers the error of
+    // test_t = T (1 - alpha) (two fp32 roundings, u = 2^-24). The reference
+    // terminates iff its test_t < floor: certain if test_t + e' < floor,
+    // certainly not if test_t - e' >= floor, otherwise the pixel is replayed.
+    const float om = 1.0f - alpha;
+    const float test_t = p.T * om;
+    const float en = fmaf(2.5f * 5.9604645e-08f, test_t, fmaf(p.eT, om, p.T * sc.x));
     const float fl = A.P.floor_f;
-    if (test_t < fmaf(fl, p.eT, fl)) {
-        if (test_t < fmaf(-fl, p.eT, fl)) {
+    if (test_t < fl + en) {
+        if (test_t < fl - en) {
             if (COUNT) p.term = static_cast<uint32_t>(jpos);
         } else {
             p.flagged = true;
@@ -285,6 +299,7 @@ __device__ __forceinline__ void blend_px(Px& p, float q, const float4& sb, const
         p.x = kNaNf; // finished
         return;
     }
+    p.eT = en;
     const float w = alpha * p.T;
     p.r = fmaf(sc.y, w, p.r);
     p.g = fmaf(sc.z, w, p.g);
@@ -295,11 +310,15 @@ __device__ __forceinline__ void blend_px(Px& p, float q, const float4& sb, const
 
 template <int KIND, int ORDER, int MODE, bool COUNT>
 __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
-    __shared__ float4 sA[kB16];
-    __shared__ float4 sB[kB16];
-    __shared__ float4 sC[kB16];
-    __shared__ float4 sD[kB16];
-    __shared__ float4 sE[kB16];
+    // Shared memory: the bucket sort's workspace; once the tile's list is
+    // sorted (it ends in sm[0, 1024)), the staging records overlay the rest.
+    using SortSm = TileSortSmem<128, 8>;
+    __shared__ __align__(16) uint32_t sm[SortSm::WORDS];
+    float4* sA = reinterpret_cast<float4*>(sm + SortSm::CAP);
+    float4* sB = sA + kB16;
+    float4* sC = sB + kB16;
+    float4* sD = sC + kB16;
+    float4* sE = sD + kB16;
 
     const FrameParams& P = A.P;
     const int tile = blockIdx.x;
@@ -321,12 +340,19 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
 
     const uint2 range = A.ranges[tile];
     const int L = static_cast<int>(range.y - range.x);
+    // the tile's list in (depth, index) order: sorted here for buckets that fit
+    // one CTA, presorted in global memory otherwise
+    const uint32_t* list = A.pval + range.x;
+    if (A.pval_w && L > 1 && L <= SortSm::CAP) {
+        list = sort_one_tile<128, 8>(range, A.pval_w, A.key, A.orig, sm);
+        __syncthreads();
+    }
     double2 pm = make_double2(0.0, 0.0);
     float4 pb0 = make_float4(0.f, 0.f, 0.f, -1.f), pb1 = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 pb2 = make_float2(0.f, 0.f);
     uint32_t pi = 0;
     if (t < L) {
-        pi = A.pval[range.x + t];
+        pi = list[t];
         pm = A.mean2d[pi];
         pb0 = A.bl0[pi];
         pb1 = A.bl1[pi];
@@ -361,7 +387,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
         __syncthreads();
         const int nb = base + kB16;
         if (nb + t < L) { // prefetch the next batch while this one is blended
-            pi = A.pval[range.x + nb + t];
+            pi = list[nb + t];
             pm = A.mean2d[pi];
             pb0 = A.bl0[pi];
             pb1 = A.bl1[pi];
@@ -454,12 +480,15 @@ void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, 
 
 } // namespace
 
-int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, DevCounters* ctr,
-                 BlendOut out, bool count_work, cudaStream_t st) {
+int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
+                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st) {
     BlendArgs a;
     a.P = P;
     a.ranges = f.ranges;
     a.pval = pair_vals;
+    a.pval_w = sort_in_place;
+    a.key = f.key;
+    a.orig = orig;
     a.mean2d = f.mean2d;
     a.bl0 = f.bl0;
     a.bl1 = f.bl1;

@@ -378,13 +378,21 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     if ((st = ensure_pairs(c, res.pairs)) != PS_OK) return st;
     f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
     const uint32_t* svals = f.pval;
+    uint32_t* sort_in_blend = nullptr;
     if (res.ctr.max_tile_len <= 16384u) {
         // K3: scatter splat indices into per-tile buckets
         launch_duplicate_buckets(f, P, n, strm);
         launches += n > 0;
         record(c, 4);
-        // K4: exact (depth, index) order inside every bucket
-        launch_tile_sort(f, s->dev.orig, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+        // K4: exact (depth, index) order inside every bucket — long buckets
+        // here, buckets of <= 1024 in the blend prologue (16x16 tiles), all of
+        // them here for the tile-list query or other tile sizes
+        if (req.mode == Mode::Render && cfg.tile_size == 16) {
+            launch_tile_sort_long(f, s->dev.orig, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+            sort_in_blend = f.pval;
+        } else {
+            launch_tile_sort(f, s->dev.orig, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+        }
         record(c, 5);
     } else {
         // Fallback for tiles longer than one CTA's shared memory: global stable
@@ -415,7 +423,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     }
     // K6: blend
     BlendOut out{req.d_rgb, req.d_t};
-    launches += launch_blend(f, P, svals, c->d_ctr, out, req.count_work, strm);
+    launches += launch_blend(f, P, svals, sort_in_blend, s->dev.orig, c->d_ctr, out, req.count_work, strm);
     record(c, 6);
     // K7: exact replay of flagged pixels (grid-stride over the device-side count)
     FrameDev fr = f;

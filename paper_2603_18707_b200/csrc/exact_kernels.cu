@@ -141,22 +141,36 @@ __device__ void blend_record(double a, double b, double c, double o, const Frame
         double dq = e32 * qb + dau + dr;
         double ref = 8.0 * e64 * (a * X * X + 2.0 * fabs(b) * X * D + c * D * D) +
                      4.0 * e64 * (a * X + fabs(b) * D) * (X + D);
-        double Gq = 4.0 * (dq + ref) + 1e-7 * qb + 1e-12;
-        // alpha error bound for the transmittance guard
+        // each term above is a first-order upper bound; 1.25 covers the
+        // second-order products, 1e-7 qb the root-finding / alpha64 rounding
+        double Gq = 1.25 * (dq + ref) + 1e-7 * qb + 1e-12;
+        // |alpha_fp32 - alpha_ref| for accepted fragments (q <= qb):
+        //   o max|k'| Gq  +  evaluation rounding  (+ ex2.approx error for exp)
         double kp = 0.5, kmag = 1.0, extra = 0.0;
         if (k.kind != PS_KERNEL_EXPONENTIAL) {
-            kp = 0.0; kmag = 0.0;
+            // max |p'(q)| over [0, qb] exactly: p' = d0 + d1 q + d2 q^2
+            const double d0 = k.order >= 1 ? k.coeffs[1] : 0.0;
+            const double d1 = k.order >= 2 ? 2.0 * k.coeffs[2] : 0.0;
+            const double d2 = k.order >= 3 ? 3.0 * k.coeffs[3] : 0.0;
+            auto dp = [&](double q) { return fabs(d0 + d1 * q + d2 * q * q); };
+            kp = fmax(dp(0.0), dp(qb));
+            if (d2 != 0.0) {
+                const double qv = -d1 / (2.0 * d2);
+                if (qv > 0.0 && qv < qb) kp = fmax(kp, dp(qv));
+            }
+            kmag = 0.0;
             double qp = 1.0;
             for (int j = 0; j <= k.order; ++j) {
                 kmag += fabs(k.coeffs[j]) * qp;
-                if (j + 1 <= k.order) kp += (j + 1) * fabs(k.coeffs[j + 1]) * qp;
                 qp *= qb;
             }
+            kmag *= 2.0 * k.order + 2.0; // folded o*c_j products + Horner FFMAs
         } else {
-            extra = amax * (4.0 * 1.1920928955078125e-07 + (0.73 * qb + 16.0) * e32);
+            // ex2.approx (2^-22) + fp32 rounding of its argument (|arg| <= 0.73 qb + |log2 o|)
+            extra = amax * (2.4e-7 + (0.73 * qb + fabs(log2(o)) + 1.0) * e32 * 0.7);
+            kmag = 0.0;
         }
-        double Ga = o * kp * Gq + 8.0 * e32 * o * kmag + extra;
-        double eTd = 2.0 * (Ga / (1.0 - amax) + 4.0 * e32);
+        const double Ga = 1.02 * (o * kp * Gq + e32 * o * kmag + extra) + 2.0 * e32 * amax + 1e-15;
         if (P.threshold_mode == kAlphaThreshold) {
             qhi = __double2float_ru(Ga);
             qlo = 0.0f;
@@ -168,7 +182,7 @@ __device__ void blend_record(double a, double b, double c, double o, const Frame
             qhi = __double2float_ru(qs + Gq);
             qlo = __double2float_rd(qs - Gq);
         }
-        eT = __double2float_ru(eTd);
+        eT = __double2float_ru(Ga);
     }
     float oval = k.kind == PS_KERNEL_EXPONENTIAL ? (o > 0.0 ? static_cast<float>(log2(o)) : -INFINITY)
                                                  : static_cast<float>(o);

@@ -53,8 +53,13 @@ struct BlendOut {
     float* rgb;
     float* t;
 };
-int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, DevCounters* ctr,
-                 BlendOut out, bool count_work, cudaStream_t st);
+// sort_in_place: buckets of <= 1024 entries still unsorted (sorted in the blend
+// prologue and written back); null when every bucket is already sorted.
+int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
+                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st);
+// sort only buckets longer than min_len (the blend prologue handles the rest)
+bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
+                           cudaStream_t st, int* launches);
 
 // utils.cu
 void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st);
