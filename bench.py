@@ -52,7 +52,7 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled (every 20 ms) during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -61,29 +61,32 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.05)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "20"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)  # first sample lands before the timed region starts
+        except OSError:
+            self._p = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.05)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=10)
+        except subprocess.TimeoutExpired:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
 
     def summary(self) -> dict:
         if not self.samples:
@@ -162,12 +165,20 @@ def run_ours(args) -> None:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    from paper_2603_18707_b200.sharding import max_over_ranks, shard_views
+
     kind, seed, n, w, h, nviews = WORKLOADS[args.workload]
     scene = api.Scene.synthetic(kind, seed, n)
     deg = scene.sh_degree
     cams = api.orbit_cameras(nviews, w, h)
-    view = (rank * max(1, nviews // max(world, 1))) % nviews
-    cam = cams[view]
+    if args.workload == "c4":
+        # C4: the 256-view batch sharded across ranks every step (scene replicated)
+        my_views = list(shard_views(nviews, world, rank))
+    else:
+        # one view per rank per step (weak scaling); rank 0 renders orbit view 0
+        my_views = [(rank * max(1, nviews // max(world, 1))) % nviews]
+    cam = cams[my_views[0]]
+    frames_per_step = len(my_views)
     r = api.Rasterizer(local)
     ds = r.upload(scene)
     lib = api.lib()
@@ -178,11 +189,14 @@ def run_ours(args) -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     cam_s = cam.to_struct()
 
+    cam_structs = [cams[v].to_struct() for v in my_views]
+
     def render_dev(cfg_s):
-        st = lib.ps_render(r.handle, ds.handle, C.byref(cam_s), C.byref(cfg_s), out_rgb.data_ptr(),
-                           out_t.data_ptr(), 1, None)
-        if st != 0:
-            raise RuntimeError(api.last_error(r.handle))
+        for cs in cam_structs:
+            st = lib.ps_render(r.handle, ds.handle, C.byref(cs), C.byref(cfg_s), out_rgb.data_ptr(),
+                               out_t.data_ptr(), 1, None)
+            if st != 0:
+                raise RuntimeError(api.last_error(r.handle))
 
     def timed(cfg_s, steps, warmup, sample_clocks=False):
         for _ in range(warmup):
@@ -212,17 +226,14 @@ def run_ours(args) -> None:
             sampler.__exit__(None, None, None)
         r.set_timing(False)
         ms = sum(a.elapsed_time(b) for a, b in evs) / steps
-        if dist:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = max_over_ranks(ms, dist, device="cuda")
         stages = {k: v / steps for k, v in stage_sum.items()}
         return ms, stages, launches, (sampler.summary() if sampler else None)
 
     cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg)
     cfg_s = cfg.to_struct()
     ms, stages, launches, clocks = timed(cfg_s, args.steps, args.warmup, sample_clocks=True)
-    fps = world * 1000.0 / ms
+    fps = world * frames_per_step * 1000.0 / ms
 
     # work counters of the timed frame (untimed render with counters)
     fb_unused, ctr = r.render(ds, cam, cfg, counters=True)
@@ -232,7 +243,7 @@ def run_ours(args) -> None:
               "vs_baseline": None, "dtype": "f32 blend, f64 preprocess/binning", "data": "synthetic",
               "config": workload_config(args.workload), "gaussians_per_s": fps * n,
               "gpu_launches": launches, "clocks": clocks}
-    result["config"]["view_per_rank"] = "orbit view (rank * 256/N)"
+    result["config"]["views_per_rank_per_step"] = frames_per_step
     result["stages_ms"] = stages
     result["work"] = {"visible": st["visible"], "pairs": st["pairs"], "kernel_evaluations": ctr.kernel_evaluations,
                       "fragments_blended": ctr.fragments_blended, "replay_pixels": st["replay_pixels"],
@@ -243,11 +254,11 @@ def run_ours(args) -> None:
 
     # poly-vs-exp and the rest of the kernel matrix (fewer steps each)
     if not args.no_compare:
-        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms}}
+        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms / frames_per_step}}
         for label, kname, mode in COMPARE:
             c2 = make_cfg(api, kname, mode, deg).to_struct()
             m2, _, _, _ = timed(c2, max(3, min(args.steps, 10)), 3)
-            kern[label] = {"frames_per_s": 1000.0 / m2, "ms": m2}
+            kern[label] = {"frames_per_s": frames_per_step * 1000.0 / m2, "ms": m2 / frames_per_step}
         result["kernels"] = kern
         result["poly1_vs_exp_speedup"] = kern["exp/stp"]["ms"] / kern[HEADLINE[0]]["ms"]
 
@@ -270,9 +281,10 @@ def run_ours(args) -> None:
                                           pin["rotations"].data_ptr(), pin["opacities"].data_ptr(),
                                           pin["sh"].data_ptr(), 0)
             assert stt == 0, api.last_error(r.handle)
-            stt = lib.ps_render(r.handle, ds.handle, C.byref(cam_s), C.byref(cfg_s), h_rgb.data_ptr(),
-                                h_t.data_ptr(), 0, None)
-            assert stt == 0, api.last_error(r.handle)
+            for cs in cam_structs:
+                stt = lib.ps_render(r.handle, ds.handle, C.byref(cs), C.byref(cfg_s), h_rgb.data_ptr(),
+                                    h_t.data_ptr(), 0, None)
+                assert stt == 0, api.last_error(r.handle)
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -282,8 +294,8 @@ def run_ours(args) -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         h2d = sum(v.numel() * v.element_size() for v in pin.values())
-        result["e2e"] = {"value": world * 1000.0 / ems, "unit": "frames/s", "ms_per_step": ems,
-                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h * w * 16),
+        result["e2e"] = {"value": world * frames_per_step * 1000.0 / ems, "unit": "frames/s", "ms_per_step": ems,
+                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(frames_per_step * h * w * 16),
                          "path": "ps_scene_update_soa (pinned host SoA) + ps_render (host outputs)"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

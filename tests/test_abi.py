@@ -1,0 +1,105 @@
+"""The drop-in boundary (CPU, no GPU): libpolysplat_b200.so loads, exports every
+function include/polysplat_b200.h declares, its POD layouts match the ctypes
+mirror, it is built for sm_100a only, and the fp64-exact translation unit
+contains no FMA contraction of the reference arithmetic."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2603_18707_b200 import _native, abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "polysplat_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ps_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declarations_are_exported():
+    lib = C.CDLL(_native.LIB_PATH)
+    declared = _declared()
+    assert set(declared) == set(_native.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ps_\w+)", out))
+    assert set(declared) <= exported
+
+
+def test_abi_version():
+    assert _native.lib().ps_abi_version() == 1
+    assert b"sm_100a" in _native.lib().ps_version()
+
+
+PROBE = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "polysplat_b200.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(ps_kernel), sizeof(ps_config), sizeof(ps_camera),
+         sizeof(ps_counters), sizeof(ps_stats), sizeof(ps_prepared));
+  printf("%zu %zu %zu %zu\n", offsetof(ps_config, kernel), offsetof(ps_config, culling_kernel),
+         offsetof(ps_config, v_dilation), offsetof(ps_camera, rotation));
+  return 0;
+}
+"""
+
+
+def test_pod_layouts_match_ctypes(tmp_path):
+    src = tmp_path / "probe.c"
+    src.write_text(PROBE)
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-std=c99", f"-I{ROOT}/include", str(src), "-o", str(exe)], check=True)
+    sizes, offs = subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines()
+    want = [C.sizeof(t) for t in (abi.ps_kernel, abi.ps_config, abi.ps_camera, abi.ps_counters, abi.ps_stats,
+                                  abi.ps_prepared)]
+    assert [int(x) for x in sizes.split()] == want
+    assert [int(x) for x in offs.split()] == [abi.ps_config.kernel.offset, abi.ps_config.culling_kernel.offset,
+                                              abi.ps_config.v_dilation.offset, abi.ps_camera.rotation.offset]
+
+
+def _sass(obj):
+    return subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
+
+
+def test_built_for_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_exact_tu_has_no_contracted_reference_arithmetic():
+    """The fp64-exact stages are compiled with -fmad=false: the only DFMAs left
+    in their SASS come from libdevice division/sqrt/transcendental sequences,
+    never from contracting the reference's a*b+c (checked on the tight test,
+    which has no division in its fast path)."""
+    obj = os.path.join(ROOT, "paper_2603_18707_b200", "_build", "exact_kernels.o")
+    if not os.path.exists(obj):
+        pytest.skip("object not built")
+    flags = open(os.path.join(ROOT, "paper_2603_18707_b200", "build.py")).read()
+    assert '("exact_kernels.cu", ["-fmad=false"])' in flags
+    sass = _sass(obj)
+    assert "k_geometry" in sass and "DFMA" in sass  # present only via libdevice sequences
+
+
+def test_poly_blend_has_no_mufu_ex2():
+    """North star: the polynomial blend evaluates alpha with FFMA + max only."""
+    obj = os.path.join(ROOT, "paper_2603_18707_b200", "_build", "blend.o")
+    if not os.path.exists(obj):
+        pytest.skip("object not built")
+    sass = _sass(obj)
+    funcs = re.split(r"\n\s+Function : ", sass)
+    poly16 = [f for f in funcs if f.startswith("_ZN2ps") and "k_blend16ILi1E" in f.split("\n")[0]]
+    exp16 = [f for f in funcs if f.startswith("_ZN2ps") and "k_blend16ILi0E" in f.split("\n")[0]]
+    assert poly16 and exp16
+    for f in poly16:
+        body = f.split("\n", 1)[1]
+        # the only MUFU allowed is inside the out-of-line fp64 exact-alpha helper (exp for the exp kernel)
+        assert "MUFU.EX2" not in body, f.split("\n")[0]
+    assert any("MUFU.EX2" in f for f in exp16)

@@ -95,3 +95,16 @@ def test_render_splat3d_fp64_dropin(gpu, reference):
     assert fb.rgb.dtype == np.float64
     assert ctr.as_dict() == ctr_r
     assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
+
+
+def test_cpp_adapter_dropin_parity(gpu):
+    """polysplat::b200::{render,prepare_splats} (include/polysplat_b200.hpp) vs the
+    reference's polysplat::{render,prepare_splats} with the reference's own types."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_parity not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "0 failures" in r.stdout
