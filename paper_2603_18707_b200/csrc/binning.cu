@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
         if (t < n_tiles) {
             ranges[t] = make_uint2(excl, excl + v);
             count[static_cast<size_t>(t)] = excl; // becomes the K3 cursor
-            if (v > 1024u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
+            if (v > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
         }
         carry += wsum[31];
         __syncthreads();
@@ -112,14 +112,14 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
                       const DevCounters* d_ctr, cudaStream_t st, int* launches) {
     if (max_len <= 1 || n_tiles == 0) return true;
     if (max_len > 16384u) return false;
-    using S1 = TileSortSmem<128, 8>;
-    k_tile_sort_small<128, 8><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key, orig);
+    using S1 = TileSortSmem<128, 16>;
+    k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key, orig);
     if (launches) *launches += 1;
-    if (max_len > 1024u) {
+    if (max_len > 2048u) {
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
         k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 1024);
+                                                                   &d_ctr->big_tiles, 2048);
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
@@ -134,12 +134,12 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
 
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches) {
-    if (max_len <= 1024u) return true;
+    if (max_len <= 2048u) return true;
     if (max_len > 16384u) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
     k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                               &d_ctr->big_tiles, 1024);
+                                                               &d_ctr->big_tiles, 2048);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 16>;

@@ -312,13 +312,21 @@ template <int KIND, int ORDER, int MODE, bool COUNT>
 __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     // Shared memory: the bucket sort's workspace; once the tile's list is
     // sorted (it ends in sm[0, 1024)), the staging records overlay the rest.
-    using SortSm = TileSortSmem<128, 8>;
-    __shared__ __align__(16) uint32_t sm[SortSm::WORDS];
-    float4* sA = reinterpret_cast<float4*>(sm + SortSm::CAP);
-    float4* sB = sA + kB16;
-    float4* sC = sB + kB16;
-    float4* sD = sC + kB16;
-    float4* sE = sD + kB16;
+    using SortSm = TileSortSmem<128, 16>;
+    union __align__(16) Smem {
+        uint32_t sort[SortSm::WORDS];
+        struct {
+            uint32_t list[SortSm::CAP]; // the sorted bucket (sort_one_tile leaves it here)
+            float4 a[kB16], b[kB16], c[kB16], d[kB16], e[kB16];
+        } st;
+    };
+    __shared__ Smem S;
+    uint32_t* sm = S.sort;
+    float4* sA = S.st.a;
+    float4* sB = S.st.b;
+    float4* sC = S.st.c;
+    float4* sD = S.st.d;
+    float4* sE = S.st.e;
 
     const FrameParams& P = A.P;
     const int tile = blockIdx.x;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     // one CTA, presorted in global memory otherwise
     const uint32_t* list = A.pval + range.x;
     if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, 8>(range, A.pval_w, A.key, A.orig, sm);
+        list = sort_one_tile<128, 16>(range, A.pval_w, A.key, A.orig, sm);
         __syncthreads();
     }
     double2 pm = make_double2(0.0, 0.0);
@@ -395,31 +403,47 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
         }
         const int cnt = min(kB16, L - base);
         if (!__any_sync(0xffffffffu, live)) continue;
-#pragma unroll
         for (int g = 0; g < kB16 / 32; ++g) {
             const int k0 = g * 32;
             if (k0 >= cnt) break;
             // warp culling: splats whose box misses this warp's 16x4 strip
             const float4 e = sE[k0 + lane];
             const bool hit = (k0 + lane < cnt) && e.x <= 15.5f && e.y >= 0.5f && e.z <= wy_hi && e.w >= wy_lo;
-            uint32_t m = __ballot_sync(0xffffffffu, hit);
-            while (m) {
-                const int k = k0 + __ffs(m) - 1;
-                m &= m - 1;
-                const float4 a = sA[k];
-                const float4 b = sB[k];
-                const float dy = yc - a.y;
-                const float mrow = fmaf(-a.w, dy, a.x);
-                const float R = b.x * dy * dy;
-                const float u0 = p0.x - mrow, u1 = p1.x - mrow;
-                const float q0 = fmaf(a.z * u0, u0, R);
-                const float q1 = fmaf(a.z * u1, u1, R);
-                const bool h0 = q0 <= b.y, h1 = q1 <= b.y;
-                if (h0 || h1) {
-                    const float4 c = sC[k];
-                    const float4 d = sD[k];
-                    if (h0) blend_px<KIND, ORDER, MODE, COUNT>(p0, q0, b, c, d, A, px0 + lx, gy, base + k, nexact);
-                    if (h1) blend_px<KIND, ORDER, MODE, COUNT>(p1, q1, b, c, d, A, px0 + lx + 8, gy, base + k, nexact);
+            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+            // phase 1: candidate bitmasks (q <= q_hi) of both pixels over the 32
+            // splats, branch-free per pixel (the per-splat skip is warp-uniform)
+            uint32_t m0 = 0u, m1 = 0u;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                if (hm & (1u << k)) {
+                    const float4 a = sA[k0 + k];
+                    const float4 b = sB[k0 + k];
+                    const float dy = yc - a.y;
+                    const float mrow = fmaf(-a.w, dy, a.x);
+                    const float R = b.x * dy * dy;
+                    const float u0 = p0.x - mrow, u1 = p1.x - mrow;
+                    const float q0 = fmaf(a.z * u0, u0, R);
+                    const float q1 = fmaf(a.z * u1, u1, R);
+                    if (q0 <= b.y) m0 |= 1u << k;
+                    if (q1 <= b.y) m1 |= 1u << k;
+                }
+            }
+            // phase 2: each pixel's candidates in list order
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                Px& p = side ? p1 : p0;
+                uint32_t m = side ? m1 : m0;
+                const int gx = px0 + lx + (side ? 8 : 0);
+                while (m) {
+                    const int k = k0 + __ffs(m) - 1;
+                    m &= m - 1;
+                    const float4 a = sA[k];
+                    const float4 b = sB[k];
+                    const float dy = yc - a.y;
+                    const float u = p.x - fmaf(-a.w, dy, a.x);
+                    const float q = fmaf(a.z * u, u, b.x * dy * dy);
+                    blend_px<KIND, ORDER, MODE, COUNT>(p, q, b, sC[k], sD[k], A, gx, gy, base + k, nexact);
+                    if (!(p.x == p.x)) m = 0u; // finished or flagged
                 }
             }
         }

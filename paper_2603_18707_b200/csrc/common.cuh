@@ -69,7 +69,7 @@ struct FrameDev {
     double2* conic_ab = nullptr;        // fp64 (a, b)
     double2* conic_cq = nullptr;        // fp64 (c, culling quadric root incl. slack)
     ushort4* rect = nullptr;            // inclusive tile rect (x0, y0, x1, y1)
-    unsigned long long* tmask = nullptr; // tight-test bits over the rect (row-major), rect <= 64 tiles
+    unsigned long long* tmask = nullptr; // tight-test bits, bit 8*(ty-y0)+(tx-x0), rects up to 8x8 tiles
     double* opacity_eff = nullptr;      // fp64 opacity_eff
     float4* bl0 = nullptr;              // fp32 blend record: A, beta, gamma, q_hi
     float4* bl1 = nullptr;              //   q_lo, o (or log2 o), eT, color r

@@ -297,14 +297,16 @@ __device__ __forceinline__ Window block_window(bool has, const int r[4], int* wb
     return w;
 }
 
+// Tight-tile masks use a fixed row stride of 8 (bit = 8 * (ty - y0) + (tx - x0)),
+// so rects of up to 8 x 8 tiles fit and bit -> tile is shifts, not divisions.
+__device__ __forceinline__ bool rect_is_small(const int r[4]) { return r[2] - r[0] < 8 && r[3] - r[1] < 8; }
+
 __device__ __forceinline__ int rect_bit_tile(const int r[4], int b, int tiles_x) {
-    const int w = r[2] - r[0] + 1;
-    return (r[1] + b / w) * tiles_x + r[0] + b % w;
+    return (r[1] + (b >> 3)) * tiles_x + r[0] + (b & 7);
 }
 
 __device__ __forceinline__ int rect_bit_win(const int r[4], int b, const Window& W) {
-    const int w = r[2] - r[0] + 1;
-    return (r[1] + b / w - W.y0) * W.w + (r[0] + b % w - W.x0);
+    return (r[1] + (b >> 3) - W.y0) * W.w + (r[0] + (b & 7) - W.x0);
 }
 
 // ------------------------------------------------------------ K1 preprocess
@@ -359,7 +361,7 @@ __device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double&
 }
 
 template <int BC>
-__global__ void __launch_bounds__(256) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
+__global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
@@ -394,14 +396,13 @@ __global__ void __launch_bounds__(256) k_geometry(SceneDev s, FrameParams P, Fra
                     coarse = static_cast<unsigned long long>(r[2] - r[0] + 1) *
                              static_cast<unsigned long long>(r[3] - r[1] + 1);
                     unsigned long long mask = 0ull;
-                    int bit = 0;
-                    const bool big = coarse > 64;
+                    const bool big = !rect_is_small(r);
                     const TightSplat tsp = make_tight(pr.conic, pr.mx, pr.my, qroot);
                     for (int ty = r[1]; ty <= r[3]; ++ty)
-                        for (int tx = r[0]; tx <= r[2]; ++tx, ++bit)
+                        for (int tx = r[0]; tx <= r[2]; ++tx)
                             if (tight_test_fast(tsp, tx, ty, ts)) {
                                 ++cnt;
-                                if (!big) mask |= 1ull << bit;
+                                if (!big) mask |= 1ull << (((ty - r[1]) << 3) + (tx - r[0]));
                                 else if (f.tile_count) atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u);
                             }
                     small = !big && cnt > 0;
@@ -540,32 +541,6 @@ __global__ void __launch_bounds__(256) k_duplicate(FrameDev f, FrameParams P, co
             }
 }
 
-// Tight tiles of splat i as tile ids, from the K1 bitmask (rect <= 64 tiles) or
-// by re-running the exact tight test (larger rects). Calls fn(tile) in the
-// rect's row-major order.
-template <class Fn>
-__device__ __forceinline__ void for_each_tight_tile(const FrameDev& f, const FrameParams& P, int64_t i, Fn&& fn) {
-    const ushort4 rc = f.rect[i];
-    const int w = rc.z - rc.x + 1, h = rc.w - rc.y + 1;
-    if (w * h <= 64) {
-        unsigned long long m = f.tmask[i];
-        while (m) {
-            const int b = __ffsll(static_cast<long long>(m)) - 1;
-            m &= m - 1;
-            fn((rc.y + b / w) * P.tiles_x + rc.x + b % w);
-        }
-        return;
-    }
-    const double2 mm = f.mean2d[i];
-    const double2 ab = f.conic_ab[i];
-    const double2 cq = f.conic_cq[i];
-    const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
-    const int ts = P.cfg.tile_size;
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-        for (int tx = rc.x; tx <= rc.z; ++tx)
-            if (tight_test_fast(t, tx, ty, ts)) fn(ty * P.tiles_x + tx);
-}
-
 // K3 (bucketed): splat indices into per-tile buckets. A CTA counts its pairs
 // per tile in the shared window, reserves one contiguous slot range per
 // distinct tile with a single global atomic, then hands out slots with shared
@@ -582,7 +557,7 @@ __global__ void __launch_bounds__(256) k_duplicate_buckets(FrameDev f, FramePara
     if (active) {
         const ushort4 rc = f.rect[i];
         r[0] = rc.x; r[1] = rc.y; r[2] = rc.z; r[3] = rc.w;
-        if ((r[2] - r[0] + 1) * (r[3] - r[1] + 1) <= 64) {
+        if (rect_is_small(r)) {
             small = true;
             m0 = f.tmask[i];
         } else { // big rect: exact tests, direct atomics (rare)

@@ -24,25 +24,24 @@ template <int THREADS, int ROUNDS>
 struct TileSortSmem {
     static constexpr int CAP = THREADS * ROUNDS;
     static constexpr int WARPS = THREADS / 32;
-    static constexpr size_t WORDS = 4 * CAP + WARPS * 256 + 2 * CAP;
-    __host__ __device__ static constexpr size_t bytes() {
-        // keys16 x2 (as u32), vals x2, full keys, per-warp digit counts
-        return sizeof(uint32_t) * (4 * CAP + WARPS * 256) + sizeof(unsigned long long) * CAP;
-    }
+    // vals [2][CAP] u32 | keys16 [2][CAP] u16 | pos [CAP] u16 | per-warp digit counts [WARPS][256] u32
+    static constexpr size_t WORDS = 2 * CAP + CAP + CAP / 2 + WARPS * 256;
+    __host__ __device__ static constexpr size_t bytes() { return sizeof(uint32_t) * WORDS; }
 };
 
-template <int THREADS, int ROUNDS>
 // Returns the sorted bucket in shared memory (smem[0, L)); also writes it back
-// to pval[r.x, r.y). Layout: vals [2][CAP] | keys16 [2][CAP] | warp counts | full keys.
+// to pval[r.x, r.y). Per-item ranks live in shared memory (not registers), so
+// ROUNDS (= CAP / THREADS) can be large without register pressure.
+template <int THREADS, int ROUNDS>
 __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __restrict__ pval,
                                                    const unsigned long long* __restrict__ key,
                                                    const uint32_t* __restrict__ orig, uint32_t* smem) {
     constexpr int WARPS = THREADS / 32;
     constexpr int CAP = THREADS * ROUNDS;
-    uint32_t* vbuf = smem;                                     // [2][CAP]
-    uint32_t* kbuf = smem + 2 * CAP;                           // [2][CAP]
-    uint32_t* whist = smem + 4 * CAP;                          // [WARPS][256]
-    unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem + 4 * CAP + WARPS * 256); // [CAP]
+    uint32_t* vbuf = smem;                                                  // [2][CAP]
+    uint16_t* kbuf = reinterpret_cast<uint16_t*>(smem + 2 * CAP);           // [2][CAP]
+    uint16_t* pos = reinterpret_cast<uint16_t*>(smem + 3 * CAP);            // [CAP]
+    uint32_t* whist = smem + 3 * CAP + CAP / 2;                             // [WARPS][256]
     __shared__ uint32_t dtot[256];
     __shared__ uint32_t wsum[WARPS];
     __shared__ unsigned long long red_min[WARPS], red_max[WARPS];
@@ -55,7 +54,6 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         const uint32_t v = pval[r.x + j];
         const unsigned long long k = key[v];
         vbuf[j] = v;
-        fk[j] = k;
         lo = min(lo, k);
         hi = max(hi, k);
     }
@@ -71,7 +69,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     for (int w = 1; w < WARPS; ++w) { lo = min(lo, red_min[w]); hi = max(hi, red_max[w]); }
     const unsigned long long span = hi - lo;
     const int shift = span ? max(0, 64 - __clzll(static_cast<long long>(span)) - 16) : 0;
-    for (int j = threadIdx.x; j < L; j += THREADS) kbuf[j] = static_cast<uint32_t>((fk[j] - lo) >> shift);
+    for (int j = threadIdx.x; j < L; j += THREADS) kbuf[j] = static_cast<uint16_t>((key[vbuf[j]] - lo) >> shift);
     const int per_warp = ((L + WARPS * 32 - 1) / (WARPS * 32)) * 32;
     uint32_t lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
@@ -80,25 +78,20 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         const int sh = pass * 8;
         for (int d = threadIdx.x; d < WARPS * 256; d += THREADS) whist[d] = 0;
         __syncthreads();
-        const uint32_t* kin = kbuf + cur * CAP;
+        const uint16_t* kin = kbuf + cur * CAP;
         const uint32_t* vin = vbuf + cur * CAP;
-        uint32_t* kout = kbuf + (cur ^ 1) * CAP;
+        uint16_t* kout = kbuf + (cur ^ 1) * CAP;
         uint32_t* vout = vbuf + (cur ^ 1) * CAP;
-        uint32_t pos[ROUNDS], dig[ROUNDS], kk[ROUNDS], vv[ROUNDS];
-#pragma unroll
-        for (int it = 0; it < ROUNDS; ++it) {
+        for (int it = 0; it < ROUNDS && it * 32 < per_warp; ++it) {
             const int j = warp * per_warp + it * 32 + lane;
-            const bool valid = (it * 32 < per_warp) && j < L;
-            kk[it] = valid ? kin[j] : 0u;
-            vv[it] = valid ? vin[j] : 0u;
-            const uint32_t d = valid ? (kk[it] >> sh) & 0xFFu : 256u;
+            const bool valid = j < L;
+            const uint32_t d = valid ? (static_cast<uint32_t>(kin[j]) >> sh) & 0xFFu : 256u;
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             const uint32_t cb = valid ? whist[warp * 256 + d] : 0u;
             __syncwarp();
             if (valid && lane == __ffs(peers) - 1) whist[warp * 256 + d] = cb + __popc(peers);
             __syncwarp();
-            pos[it] = cb + __popc(peers & lt);
-            dig[it] = d;
+            if (valid) pos[j] = static_cast<uint16_t>(cb + __popc(peers & lt));
         }
         __syncthreads();
         for (int d = threadIdx.x; d < 256; d += THREADS) {
@@ -113,36 +106,24 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         __syncthreads();
         // exclusive scan of the 256 digit totals
         constexpr int PER = 256 / THREADS > 0 ? 256 / THREADS : 1;
-        if (threadIdx.x * PER < 256) {
-            uint32_t loc[PER];
-            uint32_t sum = 0;
+        uint32_t loc[PER];
+        uint32_t sum = 0, x = 0;
+        const bool scanner = threadIdx.x * PER < 256;
+        if (scanner) {
 #pragma unroll
             for (int q = 0; q < PER; ++q) { loc[q] = dtot[threadIdx.x * PER + q]; sum += loc[q]; }
-            uint32_t x = sum;
+            x = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
             if (lane == 31) wsum[warp] = x;
-            __syncwarp();
         }
         __syncthreads();
-        if (threadIdx.x * PER < 256) {
-            uint32_t woff = 0;
-            for (int w = 0; w < warp; ++w) woff += wsum[w];
-            // recompute this thread's inclusive prefix within the warp
-            uint32_t sum = 0;
-            uint32_t loc[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) { loc[q] = dtot[threadIdx.x * PER + q]; sum += loc[q]; }
-            uint32_t x = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            uint32_t base = woff + x - sum;
+        if (scanner) {
+            uint32_t base = x - sum;
+            for (int w = 0; w < warp; ++w) base += wsum[w];
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
                 const int d = threadIdx.x * PER + q;
@@ -151,21 +132,21 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int it = 0; it < ROUNDS; ++it) {
-            if (dig[it] < 256u) {
-                const uint32_t dst = whist[warp * 256 + dig[it]] + pos[it];
-                kout[dst] = kk[it];
-                vout[dst] = vv[it];
+        for (int it = 0; it < ROUNDS && it * 32 < per_warp; ++it) {
+            const int j = warp * per_warp + it * 32 + lane;
+            if (j < L) {
+                const uint16_t k = kin[j];
+                const uint32_t dst = whist[warp * 256 + ((static_cast<uint32_t>(k) >> sh) & 0xFFu)] + pos[j];
+                kout[dst] = k;
+                vout[dst] = vin[j];
             }
         }
         __syncthreads();
         cur ^= 1;
     }
-    const uint32_t* ks = kbuf + cur * CAP;
+    const uint16_t* ks = kbuf + cur * CAP;
     uint32_t* vs = vbuf + cur * CAP;
-    // full keys in the sorted order (the fk array is indexed by original slot)
-    // -> re-gather through the value's global key
+    // ties of the 16-bit key: order each run by the full (depth bits, original index)
     for (int j = threadIdx.x; j < L; j += THREADS) {
         if ((j == 0 || ks[j - 1] != ks[j]) && j + 1 < L && ks[j + 1] == ks[j]) {
             int e = j + 1;
@@ -191,14 +172,14 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     }
     __syncthreads();
     if (need_bitonic) {
-        // degenerate depth clusters: exact bitonic sort on (bits, index)
+        // degenerate depth clusters: exact bitonic sort on (bits, original index);
+        // full keys in the (now free) second value buffer + key buffers
+        unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem + CAP);
         int n = 1;
         while (n < L) n <<= 1;
-        uint32_t* bv = vbuf + (cur ^ 1) * CAP; // free buffer (CAP >= n is not guaranteed: use fk + vs in place)
-        (void)bv;
-        for (int j = threadIdx.x; j < CAP; j += THREADS) {
+        for (int j = threadIdx.x; j < n; j += THREADS) {
             if (j < L) fk[j] = key[vs[j]];
-            else if (j < n) { fk[j] = ~0ull; vs[j] = 0xffffffffu; }
+            else { fk[j] = ~0ull; vs[j] = 0xffffffffu; }
         }
         __syncthreads();
         for (int k = 2; k <= n; k <<= 1)
@@ -209,8 +190,9 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
                     const int ix = i + jj;
                     const unsigned long long ka = fk[i], kb = fk[ix];
                     const uint32_t va = vs[i], vb = vs[ix];
-                    const bool gt = ka > kb || (ka == kb && (va == 0xffffffffu ? 0xffffffffu : orig[va]) >
-                                                                   (vb == 0xffffffffu ? 0xffffffffu : orig[vb]));
+                    const uint32_t oa = va == 0xffffffffu ? 0xffffffffu : orig[va];
+                    const uint32_t ob = vb == 0xffffffffu ? 0xffffffffu : orig[vb];
+                    const bool gt = ka > kb || (ka == kb && oa > ob);
                     if (gt == ((i & k) == 0)) { fk[i] = kb; fk[ix] = ka; vs[i] = vb; vs[ix] = va; }
                 }
                 __syncthreads();
@@ -219,6 +201,5 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     for (int j = threadIdx.x; j < L; j += THREADS) pval[r.x + j] = vs[j];
     return vs; // == smem (two passes end in buffer 0)
 }
-
 
 } // namespace ps
