@@ -423,13 +423,17 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     }
     // K6: blend
     BlendOut out{req.d_rgb, req.d_t};
-    launches += launch_blend(f, P, svals, sort_in_blend, s->dev.orig, c->d_ctr, out, req.count_work, strm);
+    bool replay_fused = false;
+    launches += launch_blend(f, P, svals, sort_in_blend, s->dev.orig, c->d_ctr, out, req.count_work, strm,
+                             &replay_fused);
     record(c, 6);
-    // K7: exact replay of flagged pixels (grid-stride over the device-side count)
-    FrameDev fr = f;
-    fr.pval = const_cast<uint32_t*>(svals);
-    launch_replay(fr, P, c->d_ctr, req.d_rgb, req.d_t, req.count_work, c->sm_count, strm);
-    launches += 1;
+    if (!replay_fused) {
+        // K7: exact replay of flagged pixels (grid-stride over the device-side count)
+        FrameDev fr = f;
+        fr.pval = const_cast<uint32_t*>(svals);
+        launch_replay(fr, P, c->d_ctr, req.d_rgb, req.d_t, req.count_work, c->sm_count, strm);
+        launches += 1;
+    }
     record(c, 7);
     CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
     CTX_TRY(c, cudaStreamSynchronize(strm));

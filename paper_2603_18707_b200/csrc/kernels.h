@@ -56,7 +56,8 @@ struct BlendOut {
 // sort_in_place: buckets of <= 1024 entries still unsorted (sorted in the blend
 // prologue and written back); null when every bucket is already sorted.
 int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
-                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st);
+                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st,
+                 bool* replay_fused);
 // sort only buckets longer than min_len (the blend prologue handles the rest)
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches);

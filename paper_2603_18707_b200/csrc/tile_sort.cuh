@@ -29,10 +29,10 @@ struct TileSortSmem {
     __host__ __device__ static constexpr size_t bytes() { return sizeof(uint32_t) * WORDS; }
 };
 
-// Returns the sorted bucket in shared memory (smem[0, L)); also writes it back
-// to pval[r.x, r.y). Per-item ranks live in shared memory (not registers), so
+// Returns the sorted bucket in shared memory (smem[0, L)); with WRITEBACK also
+// writes it back to pval[r.x, r.y). Per-item ranks live in shared memory (not registers), so
 // ROUNDS (= CAP / THREADS) can be large without register pressure.
-template <int THREADS, int ROUNDS>
+template <int THREADS, int ROUNDS, bool WRITEBACK = true>
 __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __restrict__ pval,
                                                    const unsigned long long* __restrict__ key,
                                                    const uint32_t* __restrict__ orig, uint32_t* smem) {
@@ -198,7 +198,8 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
                 __syncthreads();
             }
     }
-    for (int j = threadIdx.x; j < L; j += THREADS) pval[r.x + j] = vs[j];
+    if (WRITEBACK)
+        for (int j = threadIdx.x; j < L; j += THREADS) pval[r.x + j] = vs[j];
     return vs; // == smem (two passes end in buffer 0)
 }
 
