@@ -106,12 +106,12 @@ void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCount
 }
 
 // Bucket length <= 1024: 128 threads per tile over all tiles; longer buckets
-// (listed by k_tile_scan) by 512-thread (<= 4096) and 1024-thread (<= 16384)
-// CTAs. Longer than 16384: returns false (caller falls back).
+// (listed by k_tile_scan) by 512-thread (<= 4096) and 1024-thread (<= 12288)
+// CTAs. Longer than kMaxBucketSorted: returns false (caller falls back).
 bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint32_t max_len,
                       const DevCounters* d_ctr, cudaStream_t st, int* launches) {
     if (max_len <= 1 || n_tiles == 0) return true;
-    if (max_len > 16384u) return false;
+    if (max_len > kMaxBucketSorted) return false;
     using S1 = TileSortSmem<128, 16>;
     k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key, orig);
     if (launches) *launches += 1;
@@ -123,9 +123,9 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
-        using S3 = TileSortSmem<1024, 16>;
-        cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+        using S3 = TileSortSmem<1024, 12>;
+        cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
+        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096);
         if (launches) *launches += 1;
     }
@@ -135,16 +135,16 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches) {
     if (max_len <= 2048u) return true;
-    if (max_len > 16384u) return false;
+    if (max_len > kMaxBucketSorted) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
     k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
                                                                &d_ctr->big_tiles, 2048);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
-        using S3 = TileSortSmem<1024, 16>;
-        cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+        using S3 = TileSortSmem<1024, 12>;
+        cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
+        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096);
         if (launches) *launches += 1;
     }

@@ -481,25 +481,19 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 
 template <int KIND, int ORDER, int MODE, bool COUNT>
 __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
-    // Shared memory: the bucket sort's workspace; once the tile's list is
-    // sorted (it ends in sm[0, CAP)), the staging records overlay the rest.
     using SortSm = TileSortSmem<128, 16>;
-    union __align__(16) Smem {
-        uint32_t sort[SortSm::WORDS];
-        struct {
-            uint32_t list[SortSm::CAP]; // the sorted bucket (sort_one_tile leaves it here)
-            float4 a[kB16], b[kB16], c[kB16], d[kB16];
-            uint32_t cover[8][kB16];    // coverage word (warp * 2 + half) of each staged record
-        } st;
-    };
-    __shared__ Smem S;
+    // Shared memory: the bucket sort's workspace; the sorted list starts at word
+    // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
+    // overlay the sort's dead arrays below it.
+    __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];
-    uint32_t* sm = S.sort;
-    float4* sA = S.st.a;
-    float4* sB = S.st.b;
-    float4* sC = S.st.c;
-    float4* sD = S.st.d;
+    static_assert(4 * kB16 * 16 + 8 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
+    float4* sA = reinterpret_cast<float4*>(S);
+    float4* sB = sA + kB16;
+    float4* sC = sA + 2 * kB16;
+    float4* sD = sA + 3 * kB16;
+    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kB16); // [warp * 2 + half][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
     const FrameParams& P = A.P;
@@ -533,7 +527,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     // one CTA, presorted in global memory otherwise
     const uint32_t* list = A.pval + range.x;
     if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, 16, false>(range, A.pval_w, A.key, A.orig, sm);
+        list = sort_one_tile<128, 16, false>(range, A.pval_w, A.key, A.orig, S);
         __syncthreads();
     }
     double2 pm = make_double2(0.0, 0.0);
@@ -587,7 +581,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) S.st.cover[j][t] = cw[j];
+            for (int j = 0; j < 8; ++j) cover[j][t] = cw[j];
         }
         __syncthreads();
         const int nb = base + kB16;
@@ -607,8 +601,8 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             // block; the transpose gives lane L's pixels' masks over the 32 records
             uint32_t w0 = 0u, w1 = 0u;
             if (k0 + lane < cnt) {
-                w0 = S.st.cover[warp * 2][k0 + lane];
-                w1 = S.st.cover[warp * 2 + 1][k0 + lane];
+                w0 = cover[warp * 2][k0 + lane];
+                w1 = cover[warp * 2 + 1][k0 + lane];
             }
             if (!__any_sync(0xffffffffu, (w0 | w1) != 0u)) continue;
             uint32_t m0 = warp_transpose32(w0, tkeep, trot);

@@ -379,7 +379,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
     const uint32_t* svals = f.pval;
     uint32_t* sort_in_blend = nullptr;
-    if (res.ctr.max_tile_len <= 16384u) {
+    if (res.ctr.max_tile_len <= kMaxBucketSorted) {
         // K3: scatter splat indices into per-tile buckets
         launch_duplicate_buckets(f, P, n, strm);
         launches += n > 0;

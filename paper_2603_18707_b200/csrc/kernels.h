@@ -8,6 +8,10 @@
 
 namespace ps {
 
+// Longest per-tile bucket sorted in shared memory (binning.cu); longer tiles
+// take the global radix-sort path.
+constexpr uint32_t kMaxBucketSorted = 12288u;
+
 // exact_kernels.cu (-fmad=false)
 void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
                        cudaStream_t st);

@@ -10,197 +10,165 @@ namespace ps {
 
 // Exact per-tile order (the reference comparator, raster.cpp:172-175:
 // fp64 depth, then splat index; positive fp64 depths order like their bits):
-//  1. 16-bit key = top bits of (depth bits - tile minimum) over the tile's own
-//     depth span; stable LSD radix sort, 2 x 8-bit digits. Stable ranking: each
-//     warp owns a contiguous slice of the current order and ranks it 32 items
-//     at a time with match.any.
-//  2. every run of equal 16-bit keys is re-ordered by the full (bits, index)
-//     key; runs are expected to be ~L^2/2^17 pairs, so a thread insertion-sorts
-//     each. A run longer than kMaxRun (degenerate depth clusters) switches the
-//     CTA to a bitonic sort on the full key, which is exact for any input.
-constexpr int kMaxRun = 64;
+//  1. 32-bit key = (depth bits - tile minimum) scaled to the tile's own depth
+//     span (an order-preserving map); one counting-sort pass on its top
+//     log2(BINS) bits (shared-memory histogram + atomic cursors, so the order
+//     inside a bin is arbitrary);
+//  2. every item of a bin holding n > 1 items gets its rank inside the bin by
+//     counting the bin's items that precede it in (32-bit key, full depth bits,
+//     original index) — n compares per item, all items in parallel. A bin of
+//     more than kMaxRun items (a degenerate depth cluster) switches the CTA to
+//     a bitonic sort on the full key, which is exact for any input.
+constexpr int kMaxRun = 256;
+
+constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2_c(v >> 1); }
 
 template <int THREADS, int ROUNDS>
 struct TileSortSmem {
     static constexpr int CAP = THREADS * ROUNDS;
     static constexpr int WARPS = THREADS / 32;
-    // vals [2][CAP] u32 | keys16 [2][CAP] u16 | pos [CAP] u16 | per-warp digit counts [WARPS][256] u32
-    static constexpr size_t WORDS = 2 * CAP + CAP + CAP / 2 + WARPS * 256;
+    static constexpr int BINS = CAP >= 8192 ? 4096 : 2048;
+    static constexpr int BIN_SHIFT = 32 - ilog2_c(BINS);
+    // vin [CAP] u32 | nk [CAP] u32 | perm [CAP] u16 | dest [CAP] u16 | hist [BINS] -> sorted list [CAP]
+    static constexpr int LIST = 3 * CAP; // word offset of the sorted list
+    static constexpr size_t WORDS = LIST + (CAP > BINS ? CAP : BINS);
     __host__ __device__ static constexpr size_t bytes() { return sizeof(uint32_t) * WORDS; }
 };
 
-// Returns the sorted bucket in shared memory (smem[0, L)); with WRITEBACK also
-// writes it back to pval[r.x, r.y). Per-item ranks live in shared memory (not registers), so
-// ROUNDS (= CAP / THREADS) can be large without register pressure.
+// Returns the sorted bucket in shared memory (smem + LIST); with WRITEBACK also
+// writes it to pval[r.x, r.y). The caller synchronises before reading it.
 template <int THREADS, int ROUNDS, bool WRITEBACK = true>
 __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __restrict__ pval,
                                                    const unsigned long long* __restrict__ key,
                                                    const uint32_t* __restrict__ orig, uint32_t* smem) {
-    constexpr int WARPS = THREADS / 32;
-    constexpr int CAP = THREADS * ROUNDS;
-    uint32_t* vbuf = smem;                                                  // [2][CAP]
-    uint16_t* kbuf = reinterpret_cast<uint16_t*>(smem + 2 * CAP);           // [2][CAP]
-    uint16_t* pos = reinterpret_cast<uint16_t*>(smem + 3 * CAP);            // [CAP]
-    uint32_t* whist = smem + 3 * CAP + CAP / 2;                             // [WARPS][256]
-    __shared__ uint32_t dtot[256];
-    __shared__ uint32_t wsum[WARPS];
+    using S = TileSortSmem<THREADS, ROUNDS>;
+    constexpr int CAP = S::CAP, BINS = S::BINS, WARPS = S::WARPS, SH = S::BIN_SHIFT;
+    constexpr int PER = BINS / THREADS;
+    static_assert(BINS % (4 * THREADS) == 0 && CAP <= 65536, "tile sort shape");
+    uint32_t* vin = smem;                                             // bucket order
+    uint32_t* nk = smem + CAP;                                        // 32-bit key per bucket slot
+    uint16_t* perm = reinterpret_cast<uint16_t*>(smem + 2 * CAP);      // bin-sorted position -> slot
+    uint16_t* dest = perm + CAP;                                       // bin-sorted position -> final
+    uint32_t* hist = smem + S::LIST;                                  // counts -> cursors -> list
     __shared__ unsigned long long red_min[WARPS], red_max[WARPS];
+    __shared__ uint32_t wsum[WARPS];
     __shared__ int need_bitonic;
 
     const int L = static_cast<int>(r.y - r.x);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     unsigned long long lo = ~0ull, hi = 0ull;
-    for (int j = threadIdx.x; j < L; j += THREADS) {
+    for (int j = t; j < L; j += THREADS) {
         const uint32_t v = pval[r.x + j];
         const unsigned long long k = key[v];
-        vbuf[j] = v;
+        vin[j] = v;
         lo = min(lo, k);
         hi = max(hi, k);
     }
+    for (int d = 4 * t; d < BINS; d += 4 * THREADS) *reinterpret_cast<uint4*>(hist + d) = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
     if (lane == 0) { red_min[warp] = lo; red_max[warp] = hi; }
-    if (threadIdx.x == 0) need_bitonic = 0;
+    if (t == 0) need_bitonic = 0;
     __syncthreads();
     lo = red_min[0]; hi = red_max[0];
+#pragma unroll
     for (int w = 1; w < WARPS; ++w) { lo = min(lo, red_min[w]); hi = max(hi, red_max[w]); }
     const unsigned long long span = hi - lo;
-    const int shift = span ? max(0, 64 - __clzll(static_cast<long long>(span)) - 16) : 0;
-    for (int j = threadIdx.x; j < L; j += THREADS) kbuf[j] = static_cast<uint16_t>((key[vbuf[j]] - lo) >> shift);
-    const int per_warp = ((L + WARPS * 32 - 1) / (WARPS * 32)) * 32;
-    uint32_t lt;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    int cur = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int sh = pass * 8;
-        for (int d = threadIdx.x; d < WARPS * 256; d += THREADS) whist[d] = 0;
-        __syncthreads();
-        const uint16_t* kin = kbuf + cur * CAP;
-        const uint32_t* vin = vbuf + cur * CAP;
-        uint16_t* kout = kbuf + (cur ^ 1) * CAP;
-        uint32_t* vout = vbuf + (cur ^ 1) * CAP;
-        for (int it = 0; it < ROUNDS && it * 32 < per_warp; ++it) {
-            const int j = warp * per_warp + it * 32 + lane;
-            const bool valid = j < L;
-            const uint32_t d = valid ? (static_cast<uint32_t>(kin[j]) >> sh) & 0xFFu : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t cb = valid ? whist[warp * 256 + d] : 0u;
-            __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) whist[warp * 256 + d] = cb + __popc(peers);
-            __syncwarp();
-            if (valid) pos[j] = static_cast<uint16_t>(cb + __popc(peers & lt));
-        }
-        __syncthreads();
-        for (int d = threadIdx.x; d < 256; d += THREADS) {
-            uint32_t acc = 0;
-            for (int w = 0; w < WARPS; ++w) {
-                const uint32_t c = whist[w * 256 + d];
-                whist[w * 256 + d] = acc;
-                acc += c;
-            }
-            dtot[d] = acc;
-        }
-        __syncthreads();
-        // exclusive scan of the 256 digit totals
-        constexpr int PER = 256 / THREADS > 0 ? 256 / THREADS : 1;
-        uint32_t loc[PER];
-        uint32_t sum = 0, x = 0;
-        const bool scanner = threadIdx.x * PER < 256;
-        if (scanner) {
-#pragma unroll
-            for (int q = 0; q < PER; ++q) { loc[q] = dtot[threadIdx.x * PER + q]; sum += loc[q]; }
-            x = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) wsum[warp] = x;
-        }
-        __syncthreads();
-        if (scanner) {
-            uint32_t base = x - sum;
-            for (int w = 0; w < warp; ++w) base += wsum[w];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int d = threadIdx.x * PER + q;
-                for (int w = 0; w < WARPS; ++w) whist[w * 256 + d] += base;
-                base += loc[q];
-            }
-        }
-        __syncthreads();
-        for (int it = 0; it < ROUNDS && it * 32 < per_warp; ++it) {
-            const int j = warp * per_warp + it * 32 + lane;
-            if (j < L) {
-                const uint16_t k = kin[j];
-                const uint32_t dst = whist[warp * 256 + ((static_cast<uint32_t>(k) >> sh) & 0xFFu)] + pos[j];
-                kout[dst] = k;
-                vout[dst] = vin[j];
-            }
-        }
-        __syncthreads();
-        cur ^= 1;
-    }
-    const uint16_t* ks = kbuf + cur * CAP;
-    uint32_t* vs = vbuf + cur * CAP;
-    // ties of the 16-bit key: order each run by the full (depth bits, original index)
-    for (int j = threadIdx.x; j < L; j += THREADS) {
-        if ((j == 0 || ks[j - 1] != ks[j]) && j + 1 < L && ks[j + 1] == ks[j]) {
-            int e = j + 1;
-            while (e < L && ks[e] == ks[j] && e - j <= kMaxRun) ++e;
-            if (e - j > kMaxRun) {
-                need_bitonic = 1;
-                continue;
-            }
-            for (int a = j + 1; a < e; ++a) {
-                const uint32_t va = vs[a];
-                const unsigned long long ka = key[va];
-                int b = a - 1;
-                while (b >= j) {
-                    const uint32_t vb = vs[b];
-                    const unsigned long long kb = key[vb];
-                    if (kb < ka || (kb == ka && orig[vb] < orig[va])) break;
-                    vs[b + 1] = vb;
-                    --b;
-                }
-                vs[b + 1] = va;
-            }
-        }
+    const int nbits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+    for (int j = t; j < L; j += THREADS) {
+        const unsigned long long k = key[vin[j]] - lo;
+        const uint32_t x = nbits > 32 ? static_cast<uint32_t>(k >> (nbits - 32)) : static_cast<uint32_t>(k << (32 - nbits));
+        nk[j] = x;
+        atomicAdd(&hist[x >> SH], 1u);
     }
     __syncthreads();
-    if (need_bitonic) {
+    {   // exclusive scan of the bin counts (PER consecutive bins per thread)
+        uint32_t loc[PER];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) { loc[q] = hist[t * PER + q]; sum += loc[q]; }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        uint32_t base = x - sum;
+        for (int w = 0; w < warp; ++w) base += wsum[w];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) { hist[t * PER + q] = base; base += loc[q]; }
+    }
+    __syncthreads();
+    for (int j = t; j < L; j += THREADS) perm[atomicAdd(&hist[nk[j] >> SH], 1u)] = static_cast<uint16_t>(j);
+    __syncthreads();
+    // hist[b] is now the end of bin b: rank every item inside its bin
+    for (int p = t; p < L; p += THREADS) {
+        const uint32_t j = perm[p];
+        const uint32_t x = nk[j];
+        const uint32_t b = x >> SH;
+        const int s = b ? static_cast<int>(hist[b - 1]) : 0, e = static_cast<int>(hist[b]);
+        int rank = 0;
+        if (e - s > kMaxRun) {
+            need_bitonic = 1;
+        } else if (e - s > 1) {
+            const uint32_t v = vin[j];
+            for (int i = s; i < e; ++i) {
+                const uint32_t ji = perm[i];
+                const uint32_t xi = nk[ji];
+                bool before = xi < x;
+                if (xi == x && ji != j) {
+                    const uint32_t vi = vin[ji];
+                    const unsigned long long ki = key[vi], kv = key[v];
+                    before = ki < kv || (ki == kv && orig[vi] < orig[v]);
+                }
+                rank += before;
+            }
+        }
+        dest[p] = static_cast<uint16_t>(s + rank);
+    }
+    __syncthreads();
+    uint32_t* list = hist;
+    if (!need_bitonic) {
+        for (int p = t; p < L; p += THREADS) list[dest[p]] = vin[perm[p]];
+    } else {
         // degenerate depth clusters: exact bitonic sort on (bits, original index);
-        // full keys in the (now free) second value buffer + key buffers
-        unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem + CAP);
+        // full keys over the (now dead) vin / nk arrays
+        for (int p = t; p < L; p += THREADS) list[p] = vin[perm[p]];
+        __syncthreads();
+        unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem);
         int n = 1;
         while (n < L) n <<= 1;
-        for (int j = threadIdx.x; j < n; j += THREADS) {
-            if (j < L) fk[j] = key[vs[j]];
-            else { fk[j] = ~0ull; vs[j] = 0xffffffffu; }
+        for (int j = t; j < n; j += THREADS) {
+            if (j < L) fk[j] = key[list[j]];
+            else { fk[j] = ~0ull; list[j] = 0xffffffffu; }
         }
         __syncthreads();
         for (int k = 2; k <= n; k <<= 1)
             for (int jj = k >> 1; jj > 0; jj >>= 1) {
                 const int lg = __ffs(jj) - 1;
-                for (int p = threadIdx.x; p < (n >> 1); p += THREADS) {
-                    const int i = ((p >> lg) << (lg + 1)) + (p & (jj - 1));
+                for (int q = t; q < (n >> 1); q += THREADS) {
+                    const int i = ((q >> lg) << (lg + 1)) + (q & (jj - 1));
                     const int ix = i + jj;
                     const unsigned long long ka = fk[i], kb = fk[ix];
-                    const uint32_t va = vs[i], vb = vs[ix];
+                    const uint32_t va = list[i], vb = list[ix];
                     const uint32_t oa = va == 0xffffffffu ? 0xffffffffu : orig[va];
                     const uint32_t ob = vb == 0xffffffffu ? 0xffffffffu : orig[vb];
                     const bool gt = ka > kb || (ka == kb && oa > ob);
-                    if (gt == ((i & k) == 0)) { fk[i] = kb; fk[ix] = ka; vs[i] = vb; vs[ix] = va; }
+                    if (gt == ((i & k) == 0)) { fk[i] = kb; fk[ix] = ka; list[i] = vb; list[ix] = va; }
                 }
                 __syncthreads();
             }
     }
-    if (WRITEBACK)
-        for (int j = threadIdx.x; j < L; j += THREADS) pval[r.x + j] = vs[j];
-    return vs; // == smem (two passes end in buffer 0)
+    if (WRITEBACK) {
+        __syncthreads();
+        for (int p = t; p < L; p += THREADS) pval[r.x + p] = list[p];
+    }
+    return list;
 }
 
 } // namespace ps
