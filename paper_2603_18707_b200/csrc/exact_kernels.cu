@@ -280,12 +280,17 @@ struct Window {
 
 __device__ __forceinline__ Window block_window(bool has, const int r[4], int* wb) {
     if (threadIdx.x == 0) { wb[0] = INT_MAX; wb[1] = INT_MAX; wb[2] = -1; wb[3] = -1; }
+    // warp-reduce first: one shared atomic per warp instead of one per thread
+    const int x0 = __reduce_min_sync(0xffffffffu, has ? r[0] : INT_MAX);
+    const int y0 = __reduce_min_sync(0xffffffffu, has ? r[1] : INT_MAX);
+    const int x1 = __reduce_max_sync(0xffffffffu, has ? r[2] : -1);
+    const int y1 = __reduce_max_sync(0xffffffffu, has ? r[3] : -1);
     __syncthreads();
-    if (has) {
-        atomicMin(&wb[0], r[0]);
-        atomicMin(&wb[1], r[1]);
-        atomicMax(&wb[2], r[2]);
-        atomicMax(&wb[3], r[3]);
+    if ((threadIdx.x & 31) == 0 && x1 >= 0) {
+        atomicMin(&wb[0], x0);
+        atomicMin(&wb[1], y0);
+        atomicMax(&wb[2], x1);
+        atomicMax(&wb[3], y1);
     }
     __syncthreads();
     Window w;
@@ -546,7 +551,18 @@ __global__ void __launch_bounds__(256) k_duplicate(FrameDev f, FrameParams P, co
 // distinct tile with a single global atomic, then hands out slots with shared
 // atomics. Bucket order is arbitrary; K4 sorts each bucket by the reference's
 // exact key.
-__global__ void __launch_bounds__(256) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
+// Rects larger than 8x8 tiles (rare): exact tests, direct global atomics.
+// Out of line with scalar arguments so the common path keeps few registers.
+__device__ __noinline__ void duplicate_big(uint32_t* __restrict__ pval, uint32_t* __restrict__ tile_count,
+                                           double2 mm, double2 ab, double2 cq, int ts, int tiles_x, uint32_t i,
+                                           int r0, int r1, int r2, int r3) {
+    const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
+    for (int ty = r1; ty <= r3; ++ty)
+        for (int tx = r0; tx <= r2; ++tx)
+            if (tight_test_fast(t, tx, ty, ts)) pval[atomicAdd(&tile_count[ty * tiles_x + tx], 1u)] = i;
+}
+
+__global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -561,14 +577,8 @@ __global__ void __launch_bounds__(256) k_duplicate_buckets(FrameDev f, FramePara
             small = true;
             m0 = f.tmask[i];
         } else { // big rect: exact tests, direct atomics (rare)
-            const double2 mm = f.mean2d[i];
-            const double2 ab = f.conic_ab[i];
-            const double2 cq = f.conic_cq[i];
-            const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
-            for (int ty = r[1]; ty <= r[3]; ++ty)
-                for (int tx = r[0]; tx <= r[2]; ++tx)
-                    if (tight_test_fast(t, tx, ty, P.cfg.tile_size))
-                        f.pval[atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u)] = static_cast<uint32_t>(i);
+            duplicate_big(f.pval, f.tile_count, f.mean2d[i], f.conic_ab[i], f.conic_cq[i], P.cfg.tile_size,
+                          P.tiles_x, static_cast<uint32_t>(i), r[0], r[1], r[2], r[3]);
         }
     }
     const Window W = block_window(small, r, wb);
