@@ -199,22 +199,42 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 
 } // namespace
 
-// Tight-tile decision (raster.cpp:103-128) without per-test divisions: the
-// edge minimisers use the per-splat multipliers kx = -b/c, ky = -b/a instead of
-// ((-b)*d)/c. That perturbs the box minimum by at most ~40 ulp of
-// scale = a X^2 + 2|b| X Y + c Y^2 (X, Y = the box's largest |offsets|), so any
-// decision with |m_fast - qroot| > 1e-12 scale equals the reference's; the rest
-// re-run the reference arithmetic exactly.
+// Tight-tile decision (raster.cpp:103-128) in three tiers, each deciding only
+// what it can certify against the reference's exact fp64 result m_ref:
+//  1. fp32 screen: the same box minimum in fp32 (per-splat multipliers, FMNMX
+//     clamps). Its deviation from m_ref is < ~10u32 * scale, with
+//     scale = a X^2 + 2|b| X Y + c Y^2 (X, Y = the box's largest |offsets|):
+//     ~2u from rounding the offsets, ~5u from the products/sums, the minimiser
+//     error entering only at second order. A margin of 1e-5 scale (~170u32)
+//     plus the fp32 rounding of q_root decides all but a sliver of tests.
+//  2. fp64 without per-test divisions: the edge minimisers use kx = -b/c,
+//     ky = -b/a instead of ((-b)*d)/c, within ~40 ulp64 of scale of m_ref, so
+//     decisions with |m - q_root| > 1e-12 scale are the reference's.
+//  3. the reference arithmetic (min_quadric_over_box) for the rest.
 struct TightSplat {
     Sym2 cn;
     double mx, my, qroot, kx, ky;
+    float a32, b32, c32, kx32, ky32, q32;
+    bool screen; // fp32 tier usable (finite, non-degenerate conic)
 };
 
 __device__ __forceinline__ TightSplat make_tight(const Sym2& cn, double mx, double my, double qroot) {
-    TightSplat t{cn, mx, my, qroot, 0.0, 0.0};
+    TightSplat t{cn, mx, my, qroot, 0.0, 0.0, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, false};
     t.kx = cn.yy != 0.0 ? -cn.xy / cn.yy : 0.0;
     t.ky = cn.xx != 0.0 ? -cn.xy / cn.xx : 0.0;
+    t.a32 = static_cast<float>(cn.xx);
+    t.b32 = static_cast<float>(cn.xy);
+    t.c32 = static_cast<float>(cn.yy);
+    t.kx32 = static_cast<float>(t.kx);
+    t.ky32 = static_cast<float>(t.ky);
+    t.q32 = static_cast<float>(qroot);
+    t.screen = cn.xx != 0.0 && cn.yy != 0.0 && fabs(cn.xx) < 1e30 && fabs(cn.xy) < 1e30 && fabs(cn.yy) < 1e30 &&
+               fabs(t.kx) < 1e30 && fabs(t.ky) < 1e30 && fabs(qroot) < 1e30;
     return t;
+}
+
+__device__ __forceinline__ float quadric32(const TightSplat& t, float dx, float dy) {
+    return fmaf(t.a32 * dx, dx, fmaf(2.0f * t.b32 * dx, dy, t.c32 * dy * dy));
 }
 
 __device__ __forceinline__ bool tight_test_fast(const TightSplat& t, int tx, int ty, int ts) {
@@ -224,6 +244,21 @@ __device__ __forceinline__ bool tight_test_fast(const TightSplat& t, int tx, int
     const double lx = x0 - t.mx, hx = bx1 - t.mx;
     const double ly = y0 - t.my, hy = by1 - t.my;
     if (lx <= 0.0 && hx >= 0.0 && ly <= 0.0 && hy >= 0.0) return 0.0 <= t.qroot;
+    if (t.screen) {
+        const float flx = static_cast<float>(lx), fhx = static_cast<float>(hx);
+        const float fly = static_cast<float>(ly), fhy = static_cast<float>(hy);
+        float m = quadric32(t, flx, fminf(fmaxf(t.kx32 * flx, fly), fhy));
+        m = fminf(m, quadric32(t, fhx, fminf(fmaxf(t.kx32 * fhx, fly), fhy)));
+        m = fminf(m, quadric32(t, fminf(fmaxf(t.ky32 * fly, flx), fhx), fly));
+        m = fminf(m, quadric32(t, fminf(fmaxf(t.ky32 * fhy, flx), fhx), fhy));
+        const float X = fmaxf(fabsf(flx), fabsf(fhx)), Y = fmaxf(fabsf(fly), fabsf(fhy));
+        const float scale = fabsf(t.a32) * X * X + 2.0f * fabsf(t.b32) * X * Y + fabsf(t.c32) * Y * Y;
+        const float tol = fmaf(1e-5f, scale, fmaf(1e-6f, fabsf(t.q32), 1e-30f));
+        if (scale < 1e30f) {
+            if (m < t.q32 - tol) return true;
+            if (m > t.q32 + tol) return false;
+        }
+    }
     const Sym2& c = t.cn;
     double dy = std_clamp(c.yy != 0.0 ? t.kx * lx : ly, ly, hy);
     double m = quadric(c, lx, dy);
