@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
                                                             const unsigned long long* __restrict__ key,
                                                             const uint32_t* __restrict__ orig,
                                                             const uint32_t* __restrict__ list, const uint32_t* count,
-                                                            int min_len_exclusive) {
+                                                            int min_len_exclusive, const DevCounters* gate,
+                                                            unsigned long long pair_cap) {
     extern __shared__ uint32_t smem[];
+    if (gate && gate->pairs_total > pair_cap) return;
     const uint32_t n = *count;
     for (uint32_t q = blockIdx.x; q < n; q += gridDim.x) {
         const uint2 r = ranges[list[q]];
@@ -119,33 +121,36 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
         k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 2048);
+                                                                   &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
         k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 4096);
+                                                                   &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     return true;
 }
 
+// max_len == 0xffffffff: unknown on the host (speculative frame) -- launch both
+// list kernels; they read the device-built list and exit when it is empty.
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches) {
+    const bool unknown = max_len == 0xffffffffu;
     if (max_len <= 2048u) return true;
-    if (max_len > kMaxBucketSorted) return false;
+    if (max_len > kMaxBucketSorted && !unknown) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
     k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                               &d_ctr->big_tiles, 2048);
+                                                               &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
         k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 4096);
+                                                                   &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     return true;

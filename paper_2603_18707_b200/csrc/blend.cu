@@ -40,6 +40,8 @@ struct BlendArgs {
     uint32_t* flags;
     double4* replay_vals;              // exact (r, g, b, T) per replayed pixel (optional)
     DevCounters* ctr;
+    const DevCounters* gate;           // speculative frame: skip when pairs_total > pair_cap
+    unsigned long long pair_cap;
     float* out_rgb;
     float* out_t;
 };
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kB16); // [warp * 2 + half][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
+    if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
     const FrameParams& P = A.P;
     const int tile = blockIdx.x;
     const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
@@ -709,6 +712,8 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     a.flags = f.flags;
     a.replay_vals = f.replay_vals;
     a.ctr = ctr;
+    a.gate = f.gate;
+    a.pair_cap = f.pair_cap;
     a.out_rgb = out.rgb;
     a.out_t = out.t;
     const int ts = P.cfg.tile_size;

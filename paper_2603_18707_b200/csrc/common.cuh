@@ -85,7 +85,16 @@ struct FrameDev {
     uint32_t* tile_count = nullptr;     // pairs per tile (K1a), then the K3 bucket cursors
     uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
     double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)
+    // Speculative frames (no mid-frame host sync): the pair buffers hold
+    // pair_cap entries; kernels writing or reading them do nothing when the
+    // scan's pairs_total (in *gate) exceeds it, and the host re-runs the frame.
+    const DevCounters* gate = nullptr;
+    unsigned long long pair_cap = ~0ull;
 };
+
+__device__ __forceinline__ bool pairs_overflow(const FrameDev& f) {
+    return f.gate != nullptr && static_cast<unsigned long long>(f.gate->pairs_total) > f.pair_cap;
+}
 
 // Blend-kernel parameters derived on the host from ps_config.
 enum ThresholdMode : int {

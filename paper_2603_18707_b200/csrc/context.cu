@@ -58,6 +58,7 @@ struct ps_ctx {
     // frame scratch
     int64_t n_cap = 0;
     int64_t p_cap = 0;
+    uint32_t last_max_len = 0; // longest bucket of the last rendered frame (speculation hint)
     int64_t pix_cap = 0;
     int64_t tiles_cap = 0;
     FrameDev f;
@@ -237,6 +238,7 @@ struct FrameRequest {
     float* d_t = nullptr;
     bool count_work = false;
     bool want_replay_vals = false;
+    bool no_speculation = false; // force the synchronous (sized) path
 };
 
 struct FrameResult {
@@ -351,23 +353,81 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         launches += 1;
     }
     record(c, 2);
+    auto check_counters = [&]() -> int {
+        res.ctr = *c->h_ctr;
+        res.visible = static_cast<int64_t>(res.ctr.visible);
+        res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
+        if (res.ctr.error) {
+            uint32_t orig_index = res.ctr.error_index;
+            cudaMemcpy(&orig_index, s->dev.orig + res.ctr.error_index, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
+                          orig_index);
+            return set_err(c, static_cast<int>(res.ctr.error), buf);
+        }
+        if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
+            return set_err(c, PS_ERROR, "internal: pair scan disagrees with tight count");
+        return PS_OK;
+    };
+    auto finish_stats = [&]() {
+        c->stats.visible = res.visible;
+        c->stats.pairs = res.pairs;
+        c->stats.replay_pixels = res.ctr.replay_px;
+        c->stats.exact_alpha_evals = res.ctr.exact_evals;
+        c->stats.kernel_launches = launches;
+        if (c->timing) {
+            for (int k = 0; k < PS_STAGE_COUNT; ++k) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
+                c->stats.stage_ms[k] = ms;
+            }
+        }
+    };
+    if (req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 && !req.no_speculation &&
+        c->last_max_len <= kMaxBucketSorted) {
+        // Speculative frame: no host round trip between the count scan and the
+        // blend. The pair buffers from earlier frames are used as they are;
+        // K3 / the long-bucket sorts / the blend do nothing when this frame's
+        // pairs_total exceeds their capacity, and the host re-runs the frame
+        // (sized) after the single end-of-frame sync; likewise for a bucket
+        // longer than the shared-memory sorts take (the global-sort fallback).
+        record(c, 3);
+        f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
+        f.gate = c->d_ctr;
+        f.pair_cap = static_cast<unsigned long long>(c->p_cap);
+        launch_duplicate_buckets(f, P, n, strm);
+        launches += n > 0;
+        record(c, 4);
+        // buckets > 2048 (sorted outside the blend): launched when the last
+        // frame had any; a frame that has them unannounced is re-run
+        const bool long_sorts = c->last_max_len > 2048u;
+        if (long_sorts) launch_tile_sort_long(f, s->dev.orig, 0xffffffffu, c->d_ctr, strm, &launches);
+        record(c, 5);
+        BlendOut out{req.d_rgb, req.d_t};
+        bool replay_fused = false;
+        launches += launch_blend(f, P, f.pval, f.pval, s->dev.orig, c->d_ctr, out, req.count_work, strm,
+                                 &replay_fused);
+        record(c, 6);
+        record(c, 7);
+        CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
+        CTX_TRY(c, cudaStreamSynchronize(strm));
+        CTX_TRY(c, cudaGetLastError());
+        if ((st = check_counters()) != PS_OK) return st;
+        c->last_max_len = res.ctr.max_tile_len;
+        if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
+            (!long_sorts && res.ctr.max_tile_len > 2048u)) {
+            FrameRequest sized = req;
+            sized.no_speculation = true;
+            return run_frame(c, s, cam, cfg_in, sized, res);
+        }
+        finish_stats();
+        return PS_OK;
+    }
     CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
     CTX_TRY(c, cudaStreamSynchronize(strm));
     CTX_TRY(c, cudaGetLastError());
     record(c, 3);
-    res.ctr = *c->h_ctr;
-    res.visible = static_cast<int64_t>(res.ctr.visible);
-    res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
-    if (res.ctr.error) {
-        uint32_t orig_index = res.ctr.error_index;
-        cudaMemcpy(&orig_index, s->dev.orig + res.ctr.error_index, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-        char buf[256];
-        std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
-                      orig_index);
-        return set_err(c, static_cast<int>(res.ctr.error), buf);
-    }
-    if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
-        return set_err(c, PS_ERROR, "internal: pair scan disagrees with tight count");
+    if ((st = check_counters()) != PS_OK) return st;
     if (req.mode == Mode::CountPairs || req.mode == Mode::Prepare) {
         c->stats.visible = res.visible;
         c->stats.pairs = res.pairs;
@@ -439,18 +499,8 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     CTX_TRY(c, cudaStreamSynchronize(strm));
     CTX_TRY(c, cudaGetLastError());
     res.ctr = *c->h_ctr;
-    c->stats.visible = res.visible;
-    c->stats.pairs = res.pairs;
-    c->stats.replay_pixels = res.ctr.replay_px;
-    c->stats.exact_alpha_evals = res.ctr.exact_evals;
-    c->stats.kernel_launches = launches;
-    if (c->timing) {
-        for (int k = 0; k < PS_STAGE_COUNT; ++k) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
-            c->stats.stage_ms[k] = ms;
-        }
-    }
+    c->last_max_len = res.ctr.max_tile_len;
+    finish_stats();
     return PS_OK;
 }
 

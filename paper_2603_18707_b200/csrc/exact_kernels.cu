@@ -600,6 +600,7 @@ __device__ __noinline__ void duplicate_big(uint32_t* __restrict__ pval, uint32_t
 __global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
+    if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool active = i < n && f.tcount[i] != 0;
     int r[4] = {0, 0, -1, -1};
