@@ -18,18 +18,35 @@ namespace ps {
 namespace {
 
 constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 16; // consecutive tiles per thread per round (16K tiles per round)
 
+// One CTA: exclusive scan of the per-tile pair counts into ranges and K3
+// cursors, the total / longest bucket, and the list of buckets > 2048 (sorted
+// outside the blend). Each thread owns 16 consecutive tiles (vector loads and
+// stores), so a 1080p frame (8160 tiles) is one round.
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict__ count, uint2* __restrict__ ranges,
                                                             int n_tiles, DevCounters* ctr, uint32_t* __restrict__ big_list) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t wmax[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t carry = 0, mx = 0;
-    for (int base = 0; base < n_tiles; base += kScanThreads) {
-        const int t = base + threadIdx.x;
-        const uint32_t v = t < n_tiles ? count[static_cast<size_t>(t)] : 0u;
-        mx = max(mx, v);
-        uint32_t x = v;
+    for (int base = 0; base < n_tiles; base += kScanThreads * kScanPer) {
+        const int t0 = base + threadIdx.x * kScanPer;
+        uint32_t v[kScanPer];
+        if (t0 + kScanPer <= n_tiles) {
+#pragma unroll
+            for (int q = 0; q < kScanPer; q += 4) {
+                const uint4 x = *reinterpret_cast<const uint4*>(count + t0 + q);
+                v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kScanPer; ++q) v[q] = t0 + q < n_tiles ? count[t0 + q] : 0u;
+        }
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) { sum += v[q]; mx = max(mx, v[q]); }
+        uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -47,11 +64,32 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
             wsum[lane] = w; // inclusive over warps
         }
         __syncthreads();
-        const uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
-        if (t < n_tiles) {
-            ranges[t] = make_uint2(excl, excl + v);
-            count[static_cast<size_t>(t)] = excl; // becomes the K3 cursor
-            if (v > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
+        uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - sum;
+        if (t0 + kScanPer <= n_tiles) {
+            uint32_t cur[kScanPer];
+#pragma unroll
+            for (int q = 0; q < kScanPer; ++q) {
+                cur[q] = excl;
+                if (v[q] > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
+                excl += v[q];
+            }
+#pragma unroll
+            for (int q = 0; q < kScanPer; q += 2)
+                *reinterpret_cast<uint4*>(ranges + t0 + q) = make_uint4(cur[q], cur[q] + v[q], cur[q + 1], cur[q + 1] + v[q + 1]);
+#pragma unroll
+            for (int q = 0; q < kScanPer; q += 4) // the cursors for K3
+                *reinterpret_cast<uint4*>(count + t0 + q) = make_uint4(cur[q], cur[q + 1], cur[q + 2], cur[q + 3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kScanPer; ++q) {
+                const int t = t0 + q;
+                if (t < n_tiles) {
+                    ranges[t] = make_uint2(excl, excl + v[q]);
+                    count[t] = excl;
+                    if (v[q] > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
+                }
+                excl += v[q];
+            }
         }
         carry += wsum[31];
         __syncthreads();
