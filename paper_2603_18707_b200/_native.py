@@ -11,7 +11,8 @@ import os
 
 from . import abi
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolysplat_b200.so")
+# PS_B200_LIB: alternative build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("PS_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolysplat_b200.so")
 
 # Every function include/polysplat_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (

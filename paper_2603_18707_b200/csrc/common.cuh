@@ -6,9 +6,10 @@
 //                                     keeps the original index for the reference's
 //                                     tie-break and every output);
 //                                     fp64 SoA mean_x/y/z, scale_x/y/z, rot_w/x/y/z,
-//                                     opacity (88 B/splat) + SH as 12 float4 per splat
-//                                     sh4[i*12 + j] (the Splat3D coefficient order;
-//                                     192 B/splat at degree 3)
+//                                     opacity (88 B/splat) + SH as 12 float4 planes
+//                                     sh4[j*n + i] (plane j = floats 4j..4j+3 of the
+//                                     Splat3D coefficient order; 192 B/splat at degree 3,
+//                                     each plane read fully coalesced)
 //   frame (per render, ps_ctx):       depth keys/values for the depth sort, tight tile
 //                                     counts, fp64 mean2d / conic / culling root / rect
 //                                     (for duplicate-with-keys and the exact fp64 paths)
@@ -33,7 +34,7 @@ struct SceneDev {
     double* scale[3] = {nullptr, nullptr, nullptr};
     double* rot[4] = {nullptr, nullptr, nullptr, nullptr};
     double* opacity = nullptr;
-    float4* sh4 = nullptr; // [n][kShPlanes]
+    float4* sh4 = nullptr; // [kShPlanes][n]
     uint32_t* orig = nullptr; // internal -> original splat index (Morton order at upload)
 };
 

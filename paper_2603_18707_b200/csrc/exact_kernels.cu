@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
     float v[48];
 #pragma unroll
     for (int j = 0; j < kShPlanes; ++j) {
-        const float4 t = j < P.sh_floats4 ? s.sh4[i * kShPlanes + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 t = j < P.sh_floats4 ? s.sh4[j * s.n + i] : make_float4(0.f, 0.f, 0.f, 0.f); // plane-major: coalesced
         v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
     }
     float col[3];

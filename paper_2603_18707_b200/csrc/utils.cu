@@ -120,7 +120,7 @@ __global__ void k_gather_scene(const double* __restrict__ st, const double* __re
         s.rot[0][j] = r[0]; s.rot[1][j] = r[1]; s.rot[2][j] = r[2]; s.rot[3][j] = r[3];
         s.opacity[j] = opac[i];
 #pragma unroll
-        for (int k = 0; k < kShPlanes; ++k) s.sh4[j * kShPlanes + k] = sh[i * kShPlanes + k];
+        for (int k = 0; k < kShPlanes; ++k) s.sh4[k * n + j] = sh[i * kShPlanes + k];
         s.orig[j] = static_cast<uint32_t>(i);
     }
 }

@@ -27,7 +27,14 @@ cfg = api.RasterConfig(kernel=api.fitted_kernel(a.kernel), culling_mode=getattr(
 with api.Rasterizer(0) as r:
     ds = r.upload(scene)
     r.set_timing(True)
+    stages = []
     for _ in range(a.frames):
         fb, ctr = r.render(ds, cam, cfg, counters=False)
-        print(r.stats(), flush=True)
+        st = r.stats()
+        stages.append(st["stage_ms"])
+        print(st, flush=True)
     ds.close()
+    if a.frames >= 3:
+        import statistics
+        med = {k: round(1000 * statistics.median(s[k] for s in stages[1:]), 1) for k in stages[0]}
+        print("median stage us:", med, "sum", round(sum(med.values()), 1), flush=True)
