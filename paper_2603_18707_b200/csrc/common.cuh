@@ -6,7 +6,8 @@
 //                                     keeps the original index for the reference's
 //                                     tie-break and every output);
 //                                     fp64 SoA mean_x/y/z, scale_x/y/z, rot_w/x/y/z,
-//                                     opacity (88 B/splat) + SH as 12 float4 planes
+//                                     opacity (88 B/splat) and the camera-independent
+//                                     3D covariance (6 x fp64, computed at upload) + SH as 12 float4 planes
 //                                     sh4[j*n + i] (plane j = floats 4j..4j+3 of the
 //                                     Splat3D coefficient order; 192 B/splat at degree 3,
 //                                     each plane read fully coalesced)
@@ -33,6 +34,7 @@ struct SceneDev {
     double* mean[3] = {nullptr, nullptr, nullptr};
     double* scale[3] = {nullptr, nullptr, nullptr};
     double* rot[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* cov[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}; // 3D covariance (xx xy xz yy yz zz)
     double* opacity = nullptr;
     float4* sh4 = nullptr; // [kShPlanes][n]
     uint32_t* orig = nullptr; // internal -> original splat index (Morton order at upload)

@@ -580,6 +580,7 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
     launch_morton_order(st, n, bb, keys, vals, c->stream);
     const bool alt = radix_sort_u32(keys, keys_alt, vals, vals_alt, nullptr, n, 0, 30, scratch, c->stream, nullptr);
     launch_gather_scene(st, st + 10 * n, sh_st, alt ? vals_alt : vals, n, s->dev, c->stream);
+    launch_scene_cov(s->dev, c->stream);
     CTX_TRY(c, cudaStreamSynchronize(c->stream));
     CTX_TRY(c, cudaGetLastError());
     return PS_OK;
@@ -594,7 +595,7 @@ int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
     const size_t plane = (sizeof(double) * cap + 255) & ~size_t(255);
     const size_t shb = (sizeof(float) * 48 * cap + 255) & ~size_t(255);
     const size_t origb = (sizeof(uint32_t) * cap + 255) & ~size_t(255);
-    cudaError_t e = cudaMalloc(&s->block, 11 * plane + shb + origb);
+    cudaError_t e = cudaMalloc(&s->block, 17 * plane + shb + origb);
     if (e != cudaSuccess) {
         delete s;
         return cuda_err(c, e, "cudaMalloc(scene)");
@@ -604,6 +605,7 @@ int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
     for (int k = 0; k < 3; ++k) { s->dev.scale[k] = reinterpret_cast<double*>(p); p += plane; }
     for (int k = 0; k < 4; ++k) { s->dev.rot[k] = reinterpret_cast<double*>(p); p += plane; }
     s->dev.opacity = reinterpret_cast<double*>(p); p += plane;
+    for (int k = 0; k < 6; ++k) { s->dev.cov[k] = reinterpret_cast<double*>(p); p += plane; }
     s->dev.sh4 = reinterpret_cast<float4*>(p);
     p += shb;
     s->dev.orig = reinterpret_cast<uint32_t*>(p);

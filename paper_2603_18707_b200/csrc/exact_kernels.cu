@@ -412,11 +412,10 @@ __global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, 
         unsigned long long key = ~0ull;
         uint32_t cnt = 0;
         const double mean[3] = {s.mean[0][i], s.mean[1][i], s.mean[2][i]};
-        const double scale[3] = {s.scale[0][i], s.scale[1][i], s.scale[2][i]};
-        const double quat[4] = {s.rot[0][i], s.rot[1][i], s.rot[2][i], s.rot[3][i]};
+        const double c6[6] = {s.cov[0][i], s.cov[1][i], s.cov[2][i], s.cov[3][i], s.cov[4][i], s.cov[5][i]};
         const double opacity = s.opacity[i];
         Projected pr;
-        const int st = project(mean, scale, quat, opacity, P.cam, P.cfg.v_dilation, pr);
+        const int st = project(mean, c6, opacity, P.cam, P.cfg.v_dilation, pr);
         if (st < 0) {
             raise_error(ctr, -st, i);
         } else if (st == 0) {
@@ -732,6 +731,20 @@ __global__ void __launch_bounds__(256) k_replay(FrameDev f, FrameParams P, DevCo
     }
 }
 
+// ------------------------------------------------------------ scene covariance
+// build_covariance3d (projection.cpp:24-34) once per upload, in this -fmad=false
+// translation unit so the bits equal the reference's per-render computation.
+__global__ void __launch_bounds__(256) k_scene_cov(SceneDev s) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s.n) return;
+    const double scale[3] = {s.scale[0][i], s.scale[1][i], s.scale[2][i]};
+    const double quat[4] = {s.rot[0][i], s.rot[1][i], s.rot[2][i], s.rot[3][i]};
+    double c[9];
+    covariance3d(scale, quat, c);
+    s.cov[0][i] = c[0]; s.cov[1][i] = c[1]; s.cov[2][i] = c[2];
+    s.cov[3][i] = c[4]; s.cov[4][i] = c[5]; s.cov[5][i] = c[8];
+}
+
 // ------------------------------------------------------------ launchers
 void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
                        cudaStream_t st) {
@@ -754,6 +767,11 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
         case kBkP3: k_shade<kBkP3><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
         default: k_shade<kBkGeneric><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
     }
+}
+
+void launch_scene_cov(const SceneDev& s, cudaStream_t st) {
+    if (s.n == 0) return;
+    k_scene_cov<<<static_cast<int>((s.n + 255) / 256), 256, 0, st>>>(s);
 }
 
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,

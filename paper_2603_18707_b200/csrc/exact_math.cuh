@@ -100,8 +100,11 @@ struct Projected {
 // projection.cpp:36-79 project_splat (geometry part; the SH colour of :77 is
 // evaluated separately in fp32). Returns 1 visible, 0 behind the near plane,
 // -PS_DEGENERATE_COVARIANCE when det(cov_aa) <= 1e-12.
-PS_HD int project(const double mean[3], const double scale[3], const double quat[4], double opacity,
-                  const ps_camera& cam, double v, Projected& out) {
+// cov3d: the 3D covariance of covariance3d(scale, quat) as its 6 distinct
+// entries (xx, xy, xz, yy, yz, zz). It does not depend on the camera, so the
+// scene stores it (computed once per upload with this same arithmetic).
+PS_HD int project(const double mean[3], const double c6[6], double opacity, const ps_camera& cam, double v,
+                  Projected& out) {
     const double* R = cam.rotation;
     const double* t = cam.translation;
     double px = R[0] * mean[0] + R[1] * mean[1] + R[2] * mean[2];
@@ -122,8 +125,7 @@ PS_HD int project(const double mean[3], const double scale[3], const double quat
         m0[j] = jr0[0] * R[0 * 3 + j] + jr0[1] * R[1 * 3 + j] + jr0[2] * R[2 * 3 + j];
         m1[j] = jr1[0] * R[0 * 3 + j] + jr1[1] * R[1 * 3 + j] + jr1[2] * R[2 * 3 + j];
     }
-    double cov3d[9];
-    covariance3d(scale, quat, cov3d);
+    const double cov3d[9] = {c6[0], c6[1], c6[2], c6[1], c6[3], c6[4], c6[2], c6[4], c6[5]};
     double t0[3], t1[3];
     for (int j = 0; j < 3; ++j) {
         t0[j] = m0[0] * cov3d[0 * 3 + j] + m0[1] * cov3d[1 * 3 + j] + m0[2] * cov3d[2 * 3 + j];

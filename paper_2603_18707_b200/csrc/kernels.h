@@ -15,6 +15,8 @@ constexpr uint32_t kMaxBucketSorted = 12288u;
 // exact_kernels.cu (-fmad=false)
 void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
                        cudaStream_t st);
+// camera-independent 3D covariance of every splat (after each upload)
+void launch_scene_cov(const SceneDev& s, cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
                       cudaStream_t st);
 void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
