@@ -388,10 +388,38 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
     top = dict(out[dom]) if dom else {}
     if dom:
         top["kernel"] = dom
-        top["traffic"] = None
+        top["traffic"], top["traffic_source"] = profiled_traffic(dom, kname)
         top["peak_note"] = ("HBM peak from MEASURED_PEAKS.json" if top["bound"] == "hbm"
                             else "FP32 issue peak measured in-run (no FP32 entry in MEASURED_PEAKS.json)")
     return top, out
+
+
+# stage -> kernel-name prefix in the ncu captures (blend: the 16x16 kernel of the headline kernel class)
+_STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0", "preprocess": "k_geometry", "duplicate": "k_duplicate_buckets"}
+
+
+def profiled_traffic(stage: str, kname: str):
+    """DRAM bytes (read + write) per launch of the stage's kernel, from the
+    newest committed `ncu --set full` capture of C2 (profiles/*_ncu_full_c2_raw.csv),
+    or (None, reason)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full_c2_raw.csv")))
+    if not files or kname != "poly1" or stage not in _STAGE_KERNEL:
+        return None, "no matching ncu capture"
+    rows = list(csv.reader(open(files[-1])))
+    hdr, units = rows[0], rows[1]
+    try:
+        ki, ri, wi = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    except ValueError:
+        return None, "capture lacks dram__bytes metrics"
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[2:]:
+        if _STAGE_KERNEL[stage] in r[ki]:
+            b = float(r[ri].replace(",", "")) * scale.get(units[ri], 1.0) + \
+                float(r[wi].replace(",", "")) * scale.get(units[wi], 1.0)
+            return b, f"{os.path.basename(files[-1])} ({r[ki].split('(')[0]})"
+    return None, "kernel not in capture"
 
 
 def cpu_baseline(workload: str) -> dict:
