@@ -338,7 +338,7 @@ def run_ours(args) -> None:
                                  "2 host threads x 2 contexts, device-timed over all frames"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args.workload)
+        result["cpu_baseline"] = cpu_baseline(args.workload, (fb_unused, ctr))
 
     ds.close()
     r.close()
@@ -422,8 +422,26 @@ def profiled_traffic(stage: str, kname: str):
     return None, "kernel not in capture"
 
 
-def cpu_baseline(workload: str) -> dict:
-    """The reference's own renderer (oracle/_ref) on this host, bounded sample."""
+def full_size_parity(ours, ref_out) -> dict:
+    """Our timed frame vs the reference's image of the same frame: max-abs per
+    channel and transmittance, PSNR of the white-background composite
+    (metrics.cpp:13-44), and the six work counters."""
+    import numpy as np
+    fb, ctr = ours
+    rgb, tr, ctr_ref = ref_out
+    d_rgb = float(np.max(np.abs(fb.rgb.astype(np.float64) - rgb)))
+    d_t = float(np.max(np.abs(fb.transmittance.astype(np.float64) - tr)))
+    ca = fb.rgb.astype(np.float64) + fb.transmittance.astype(np.float64)[..., None]
+    cb = rgb + tr[..., None]
+    mse = float(np.mean((ca - cb) ** 2))
+    return {"max_abs_rgb": d_rgb, "max_abs_t": d_t, "tolerance": 1e-5,
+            "psnr_db": None if mse == 0.0 else 10.0 * float(np.log10(1.0 / mse)),
+            "counters_identical": ctr.as_dict() == ctr_ref}
+
+
+def cpu_baseline(workload: str, ours=None) -> dict:
+    """The reference's own renderer (oracle/_ref) on this host, bounded sample;
+    its image of the frame also checks our timed frame at full size."""
     try:
         from oracle import oracle
         from paper_2603_18707_b200 import api
@@ -432,14 +450,15 @@ def cpu_baseline(workload: str) -> dict:
         splats, deg = api.synthetic_splat3d({"g": 3, "skewed": 4}[kind], seed, n)
         cam = api.orbit_cameras(256, w, h)[0].to_struct()
         cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg).to_struct()
-        ref.render(splats, cam, cfg)  # warm-up
+        ref_out = ref.render(splats, cam, cfg)  # warm-up (its image is the parity check)
         ts = []
         for _ in range(3):
             t0 = time.perf_counter()
             ref.render(splats, cam, cfg)
             ts.append(time.perf_counter() - t0)
         ms = 1000.0 * statistics.median(ts)
-        return {"value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0), "kind": "reference",
+        parity = full_size_parity(ours, ref_out) if ours is not None else None
+        return {"parity": parity, "value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0), "kind": "reference",
                 "ms_per_frame": ms, "sample": f"median of 3 full {workload.upper()} frames ({HEADLINE[0]}), "
                                                "polysplat::render built from the reference sources, all host threads"}
     except Exception as e:  # noqa: BLE001

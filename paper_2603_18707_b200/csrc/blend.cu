@@ -228,28 +228,24 @@ __global__ void k_blend(const BlendArgs A) {
 
 // ---------------------------------------------------------------- 16x16 fast path
 // tile_size == 16: 128 threads; warp w owns the 8x8 block (w & 1, w >> 1) of the
-// tile, lane L the pixels (L & 7, L >> 3) and (L & 7, 4 + (L >> 3)) of it.
+// tile, lane L the horizontal pixel PAIR (2 (L & 3), 2 (L & 3) + 1) of block row
+// L >> 2. Both pixels of a pair walk the same records: one record load, one
+// set of row terms (dy, row centre, gamma dy^2) per step, and the per-pixel
+// arithmetic in packed f32x2 (FFMA2 / FMUL2 / FADD2 with broadcast operands).
 // Batches of 128 records live in static shared memory and the next batch is
 // prefetched into registers while the current one is blended. While staging a
 // record, its thread also computes a conservative coverage mask of
-// {q <= q_hi} over the tile's 256 pixel centres (one x-interval per row);
-// per group of 32 records a warp bit-transposes its block's masks into one
-// 32-record candidate mask per pixel, then walks both pixels' candidates in
-// list order, one of each per step, re-deciding q <= q_hi exactly. A finished
-// pixel gets x = NaN, so its later tests fail without a branch. Pixels whose
+// {q <= q_hi} over the tile's 128 pixel pairs (one x-interval per row, widened
+// to whole pairs); per group of 32 records each warp bit-transposes its
+// block's words into one 32-record candidate mask per pair, then walks it in
+// list order, re-deciding q <= q_hi exactly for each pixel. A finished pixel
+// gets x = NaN, so its later tests fail without a branch. Pixels whose
 // decisions the fp32 error bounds cannot certify are replayed at the end of the
 // CTA in exact fp64 from the tile's sorted list.
 constexpr int kB16 = 128;
 constexpr float kNaNf = __builtin_nanf("");
 // byte offsets of the record planes a, b, c, d in the staging area
 constexpr uint32_t kOffB = kB16 * 16, kOffC = 2 * kB16 * 16, kOffD = 3 * kB16 * 16;
-
-struct Px {
-    float x;      // tile-local pixel-centre x (NaN once the pixel is finished)
-    float T, r, g, b, eT;
-    uint32_t term, nbl;
-    uint32_t flagged;
-};
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
     float4 v;
@@ -286,13 +282,54 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const uint32_t 
     return x;
 }
 
+// ---- packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2; scalars broadcast as .F32 operands)
+struct F2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ F2 f2(float lo, float hi) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ F2 f2b(float s) { return f2(s, s); }
+__device__ __forceinline__ float f2lo(F2 a) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+    return lo;
+}
+__device__ __forceinline__ float f2hi(F2 a) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+    return hi;
+}
+__device__ __forceinline__ F2 f2add(F2 a, F2 b) {
+    F2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 f2sub(F2 a, F2 b) {
+    F2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 f2mul(F2 a, F2 b) {
+    F2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 f2fma(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+
 // Conservative coverage of {q <= q_hi} over the 16 pixel centres of tile row
-// `row`, as a 16-bit mask. Every pixel whose fp32 quadric (cand_step's exact
-// expression, same dy and row centre) is <= q_hi is included: q_hi is inflated
-// by the quadric's rounding (~5u relative) and the half-width by the
-// approximate rcp/sqrt error plus an absolute margin; a pixel included in
-// excess only costs one re-decided candidate step.
-__device__ __forceinline__ uint32_t row_cover(int row, float mx, float my, float beta, float gamma, float qpad,
+// `row`, widened to the row's 8 pixel pairs (bit k = pair (2k, 2k+1)). Every
+// pixel whose fp32 quadric (the walk's exact expression, same dy and row
+// centre) is <= q_hi is included: q_hi is inflated by the quadric's rounding
+// (~5u relative) and the half-width by the approximate rcp/sqrt error plus an
+// absolute margin; a pair included in excess only costs one skipped step.
+__device__ __forceinline__ uint32_t row_pairs(int row, float mx, float my, float beta, float gamma, float qpad,
                                               float ia) {
     const float dy = (row + 0.5f) - my;
     const float rhs = fmaf(-gamma * dy, dy, qpad);
@@ -300,87 +337,159 @@ __device__ __forceinline__ uint32_t row_cover(int row, float mx, float my, float
     float h = sqrt_approx(fmaxf(rhs, 0.0f) * ia);
     h = fmaf(h, 1.00002f, fmaf(fabsf(mr), 2e-6f, 1e-3f));
     if (!(rhs >= 0.0f)) h = -1.0f; // empty row
-    const int lo = min(max(__float2int_ru(mr - h - 0.5f), 0), 16);
-    const int hi = max(min(__float2int_rd(mr + h - 0.5f), 15), -1);
-    return (0xFFFFu << lo) & (0xFFFFu >> (15 - hi));
+    const int lo = min(max(__float2int_ru(mr - h - 0.5f), 0), 16) >> 1;
+    const int hi = max(min(__float2int_rd(mr + h - 0.5f), 15), -2) >> 1;
+    return (0xFFu << lo) & (0xFFu >> (7 - hi));
 }
 
 // Shared-memory record of one staged splat (tile-local, fp32):
-//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, K0}  c = {g_alpha, r, g, b}
-//   d = {K1, K2, K3, splat index bits}   e = {x_lo, x_hi, y_lo, y_hi}
-// K_j = o c_j folds the opacity into the polynomial (K0 = log2 o for exp);
-// e is the axis-aligned extent of {q <= q_hi} (+ margin) used for warp culling.
+//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, g'}  c = {-K0, -r, -g, -b}
+//   d = {-K1, -K2, -K3, -}
+// K_j = o c_j folds the opacity into the polynomial (c.x = log2 o for exp; -o
+// in alpha-threshold mode). The walk carries NEGATED alphas (-alpha = Horner
+// over the negated coefficients, exactly), so that T' = fma(-alpha, T, T) is
+// one rounding and the colour update fma(-alpha T, -c, rgb) needs no negation.
+// g' = 1.001 (g + 2.2u) + 4u64 widens g = the splat's |alpha_fp32 - alpha_ref|
+// bound (u = 2^-24, u64 = 2^-53) for the interval update below.
 //
-// One candidate (q <= q_hi) of pixel p, at list position jpos; v = lane has one.
+// Per-pair state of the walk. Invariant: for each live pixel, the reference's
+// fp64 transmittance lies in [Lo, Up]. A blend of a fragment with fp32 alpha a
+// (so alpha_ref in [a - g, a + g]) maps it to
+//     Up' = fma(Up, g', fma(-a, Up, Up)),   Lo' = fma(Lo, -g', fma(-a, Lo, Lo))
+// (each inner fma is Up (1 - a) with one rounding; g' covers both fp32
+// roundings and the reference's two fp64 roundings), so the reference's
+// test_t < floor is certainly false when Lo' >= floor and certainly true when
+// Up' < floor; only the band between is undecided (exact replay). T itself is
+// the fp32 value blended with (T' = fma(-a, T, T)).
+struct Pair {
+    F2 x;                   // tile-local pixel-centre x of both pixels (NaN once finished)
+    F2 T, Up, Lo, r, g, b;
+    uint32_t term0, term1;  // list position of the terminating fragment (COUNT)
+    uint32_t nbl0, nbl1;    // fragments blended (COUNT)
+    uint32_t flag;          // bit p: pixel p needs the exact replay
+};
+
+// One record (staged at shared address rec, list position jpos) for both pixels
+// of the pair at row centre yc. m: the pair's remaining candidates (cleared
+// when both pixels are finished).
 template <int KIND, int ORDER, int MODE, bool COUNT>
-__device__ __forceinline__ void cand_step(Px& p, bool v, uint32_t rec, float yc, const FrameParams& P, int jpos) {
+__device__ __forceinline__ void pair_step(Pair& p, uint32_t rec, float yc, const FrameParams& P, int jpos,
+                                          uint32_t& m) {
     const float4 a = lds128(rec);
     const float4 b = lds128(rec + kOffB);
     const float4 c = lds128(rec + kOffC);
     const float dy = yc - a.y;
-    const float u = p.x - fmaf(-a.w, dy, a.x);
-    const float q = fmaf(a.z * u, u, b.x * dy * dy);
-    float alpha;
-    bool amb, skip = false;
+    const float mr = fmaf(-a.w, dy, a.x);
+    const float cr = b.x * dy * dy;
+    const F2 u = f2sub(p.x, f2b(mr));
+    const F2 q = f2fma(f2mul(u, f2b(a.z)), u, f2b(cr));
+    const float q0 = f2lo(q), q1 = f2hi(q);
+    float n0, n1; // -alpha
+    bool skip0, skip1, amb;
     if (MODE == kQuadricThreshold) {
-        // the coverage masks are a superset: q > q_hi is a certain skip
-        skip = !(q <= b.y);
-        // q in the certified band [q_lo, q_hi]: the reference's alpha < eps is
-        // undecided in fp32 -> exact replay of the pixel
-        amb = q >= b.z;
-        // accepted fragments have q < q* + Gq < first_root, where the ReLU /
-        // piecewise cut-offs are inactive: alpha = min(.999, sum K_j q^j)
+        // the coverage masks are a superset: q > q_hi is a certain skip; q in
+        // the certified band [q_lo, q_hi] leaves the reference's alpha < eps
+        // undecided in fp32 -> exact replay of the pixel. Accepted fragments
+        // have q < q* + Gq < first_root, where the ReLU / piecewise cut-offs
+        // are inactive: alpha = min(.999, sum K_j q^j)
+        skip0 = !(q0 <= b.y);
+        skip1 = !(q1 <= b.y);
+        amb = ((q0 >= b.z) & !skip0) | ((q1 >= b.z) & !skip1);
+        F2 na;
         if (KIND == 0) {
-            alpha = fminf(0.999f, ex2_approx(fmaf(q, -0.72134752044448170f, b.w)));
+            const F2 ar = f2fma(q, f2b(-0.72134752044448170f), f2b(c.x));
+            na = f2(-ex2_approx(f2lo(ar)), -ex2_approx(f2hi(ar)));
+        } else if (ORDER == 1) {
+            na = f2fma(q, f2b(lds32(rec + kOffD)), f2b(c.x));
         } else {
-            float pq;
-            if (ORDER == 1) {
-                pq = lds32(rec + kOffD);
-            } else {
-                const float4 d = lds128(rec + kOffD);
-                pq = ORDER == 2 ? d.y : d.z;
-                if (ORDER >= 3) pq = fmaf(pq, q, d.y);
-                pq = fmaf(pq, q, d.x);
-            }
-            alpha = fminf(0.999f, fmaf(pq, q, b.w));
+            const float4 d = lds128(rec + kOffD);
+            F2 pq = f2b(ORDER == 2 ? d.y : d.z);
+            if (ORDER >= 3) pq = f2fma(pq, q, f2b(d.y));
+            pq = f2fma(pq, q, f2b(d.x));
+            na = f2fma(pq, q, f2b(c.x));
         }
+        n0 = fmaxf(-0.999f, f2lo(na));
+        n1 = fmaxf(-0.999f, f2hi(na));
     } else {
         // non-monotone kernel: full ReLU / piecewise semantics, guard on alpha
         const KernelF32& kf = P.kf;
-        float pq = kf.c[kf.order];
-        for (int j = kf.order - 1; j >= 0; --j) pq = fmaf(pq, q, kf.c[j]);
-        if (kf.kind == PS_KERNEL_POLY_PIECEWISE && !(q < kf.first_root)) pq = 0.0f;
-        alpha = KIND == 0 ? fminf(0.999f, ex2_approx(fmaf(q, -0.72134752044448170f, b.w)))
-                          : fminf(0.999f, fmaxf(b.w * pq, 0.0f)); // K0 = o here
-        skip = alpha < P.eps_f - b.y;
-        amb = !skip && alpha < P.eps_f + b.y;
-    }
-    // Transmittance decision (raster.cpp:272-277) with a running ABSOLUTE error
-    // bound e >= |T_fp32 - T_ref|: with g = the splat's |alpha_fp32 - alpha_ref|
-    // bound (c.x), e' = e (1 - alpha) + T g + 2.5u T' covers the error of
-    // test_t = T (1 - alpha) (two fp32 roundings, u = 2^-24). The reference
-    // terminates iff its test_t < floor: certain if test_t + e' < floor,
-    // certainly not if test_t - e' >= floor, otherwise the pixel is replayed.
-    const float om = 1.0f - alpha;
-    const float tt = p.T * om;
-    const float en = fmaf(2.5f * 5.9604645e-08f, tt, fmaf(p.eT, om, p.T * c.x));
-    const float fl = P.floor_f;
-    const bool live = v && !skip;
-    if (__builtin_expect(live && (amb || tt < fl + en), 0)) {
-        if (!amb && tt < fl - en) {
-            if (COUNT) p.term = static_cast<uint32_t>(jpos);
+        float a0, a1;
+        if (KIND == 0) {
+            a0 = ex2_approx(fmaf(q0, -0.72134752044448170f, c.x));
+            a1 = ex2_approx(fmaf(q1, -0.72134752044448170f, c.x));
         } else {
-            p.flagged = 1u;
+            F2 pq = f2b(kf.c[kf.order]);
+            for (int j = kf.order - 1; j >= 0; --j) pq = f2fma(pq, q, f2b(kf.c[j]));
+            a0 = f2lo(pq), a1 = f2hi(pq);
+            if (kf.kind == PS_KERNEL_POLY_PIECEWISE) {
+                if (!(q0 < kf.first_root)) a0 = 0.0f;
+                if (!(q1 < kf.first_root)) a1 = 0.0f;
+            }
+            a0 = fmaxf(-c.x * a0, 0.0f);
+            a1 = fmaxf(-c.x * a1, 0.0f);
         }
-        p.x = kNaNf; // finished
-    } else if (live) {
-        p.eT = en;
-        const float w = alpha * p.T;
-        p.r = fmaf(c.y, w, p.r);
-        p.g = fmaf(c.z, w, p.g);
-        p.b = fmaf(c.w, w, p.b);
-        p.T = tt;
-        if (COUNT) ++p.nbl;
+        const float ga = b.y; // |alpha_fp32 - alpha_ref| bound in this mode
+        a0 = fminf(0.999f, a0);
+        a1 = fminf(0.999f, a1);
+        skip0 = !(a0 >= P.eps_f - ga);
+        skip1 = !(a1 >= P.eps_f - ga);
+        amb = ((a0 < P.eps_f + ga) & !skip0) | ((a1 < P.eps_f + ga) & !skip1);
+        n0 = -a0;
+        n1 = -a1;
+    }
+    float g0 = b.w, g1 = b.w;
+    if (skip0) { n0 = 0.0f; g0 = 0.0f; }
+    if (skip1) { n1 = 0.0f; g1 = 0.0f; }
+    F2 na = f2(n0, n1);
+    const F2 gp = f2(g0, g1);
+    F2 tt = f2fma(na, p.T, p.T); // T (1 - alpha), one rounding; == T when skipped
+    const F2 up = f2fma(p.Up, gp, f2fma(na, p.Up, p.Up));
+    F2 lo = f2fma(p.Lo, f2mul(gp, f2b(-1.0f)), f2fma(na, p.Lo, p.Lo));
+    // Transmittance decision (raster.cpp:272-277): the reference terminates iff
+    // its test_t < floor; Lo' >= floor certifies it does not (the common case,
+    // no branch); otherwise decide per pixel below.
+    const float fl = P.floor_f;
+    if (__builtin_expect(amb | (fminf(f2lo(lo), f2hi(lo)) < fl), 0)) {
+        const F2 hi = up; // < floor: certainly below it
+        float x0 = f2lo(p.x), x1 = f2hi(p.x);
+        bool done0 = false, done1 = false;
+        if (!skip0) {
+            const bool amb0 = MODE == kQuadricThreshold ? q0 >= b.z : -n0 < P.eps_f + b.y;
+            if (amb0 || f2lo(lo) < fl) {
+                done0 = true;
+                if (!amb0 && f2lo(hi) < fl) { if (COUNT) p.term0 = static_cast<uint32_t>(jpos); }
+                else p.flag |= 1u;
+            }
+        }
+        if (!skip1) {
+            const bool amb1 = MODE == kQuadricThreshold ? q1 >= b.z : -n1 < P.eps_f + b.y;
+            if (amb1 || f2hi(lo) < fl) {
+                done1 = true;
+                if (!amb1 && f2hi(hi) < fl) { if (COUNT) p.term1 = static_cast<uint32_t>(jpos); }
+                else p.flag |= 2u;
+            }
+        }
+        // a finished pixel does not blend this fragment and keeps its T (alpha
+        // = 0 below); a huge Lo keeps it out of this branch from now on
+        float l0 = f2lo(lo), l1 = f2hi(lo);
+        if (done0) { n0 = 0.0f; x0 = kNaNf; skip0 = true; l0 = 3.0e38f; }
+        if (done1) { n1 = 0.0f; x1 = kNaNf; skip1 = true; l1 = 3.0e38f; }
+        p.x = f2(x0, x1);
+        na = f2(n0, n1);
+        tt = f2fma(na, p.T, p.T);
+        lo = f2(l0, l1);
+        if (x0 != x0 && x1 != x1) m = 0u; // both pixels finished
+    }
+    const F2 w = f2mul(na, p.T); // -alpha T
+    p.r = f2fma(w, f2b(c.y), p.r);
+    p.g = f2fma(w, f2b(c.z), p.g);
+    p.b = f2fma(w, f2b(c.w), p.b);
+    p.T = tt;
+    p.Up = up;
+    p.Lo = lo;
+    if (COUNT) {
+        p.nbl0 += skip0 ? 0u : 1u;
+        p.nbl1 += skip1 ? 0u : 1u;
     }
 }
 
@@ -490,12 +599,12 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];
-    static_assert(4 * kB16 * 16 + 8 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
+    static_assert(4 * kB16 * 16 + 4 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
     float4* sA = reinterpret_cast<float4*>(S);
     float4* sB = sA + kB16;
     float4* sC = sA + 2 * kB16;
     float4* sD = sA + 3 * kB16;
-    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kB16); // [warp * 2 + half][record]
+    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kB16); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
     if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
@@ -506,13 +615,19 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     const int px0 = tx * 16, py0 = ty * 16;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
-    const int lx = ((warp & 1) << 3) + (lane & 7);      // both pixels' column
-    const int ly0 = ((warp >> 1) << 3) + (lane >> 3);   // first pixel's row; second: ly0 + 4
-    const float yc0 = ly0 + 0.5f, yc1 = ly0 + 4.5f;
-    const bool col_in = px0 + lx < W;
-    Px p0{(col_in && py0 + ly0 < H) ? lx + 0.5f : kNaNf, 1.f, 0.f, 0.f, 0.f, 0.f, 0xffffffffu, 0u, 0u};
-    Px p1{(col_in && py0 + ly0 + 4 < H) ? lx + 0.5f : kNaNf, 1.f, 0.f, 0.f, 0.f, 0.f, 0xffffffffu, 0u, 0u};
-    const bool in0 = p0.x == p0.x, in1 = p1.x == p1.x;
+    const int lx = ((warp & 1) << 3) + ((lane & 3) << 1); // left pixel's column; right: lx + 1
+    const int ly = ((warp >> 1) << 3) + (lane >> 2);      // the pair's row
+    const float yc = ly + 0.5f;
+    const bool row_in = py0 + ly < H;
+    const bool in0 = row_in && px0 + lx < W, in1 = row_in && px0 + lx + 1 < W;
+    Pair p;
+    p.x = f2(in0 ? lx + 0.5f : kNaNf, in1 ? lx + 1.5f : kNaNf);
+    p.T = f2b(1.0f);
+    p.Up = p.Lo = f2b(1.0f);
+    p.r = p.g = p.b = f2b(0.0f);
+    p.term0 = p.term1 = 0xffffffffu;
+    p.nbl0 = p.nbl1 = 0u;
+    p.flag = 0u;
     const float c0 = P.kf.c[0], c1 = P.kf.c[1], c2 = P.kf.c[2], c3 = P.kf.c[3];
     uint32_t tkeep[5], trot[5];
 #pragma unroll
@@ -536,60 +651,56 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     double2 pm = make_double2(0.0, 0.0);
     float4 pb0 = make_float4(0.f, 0.f, 0.f, -1.f), pb1 = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 pb2 = make_float2(0.f, 0.f);
-    uint32_t pi = 0;
     if (t < L) {
-        pi = list[t];
+        const uint32_t pi = list[t];
         pm = A.mean2d[pi];
         pb0 = A.bl0[pi];
         pb1 = A.bl1[pi];
         pb2 = A.bl2[pi];
     }
     for (int base = 0; base < L; base += kB16) {
-        const bool live = (p0.x == p0.x) || (p1.x == p1.x);
+        const bool live = (f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x));
         if (__syncthreads_count(live) == 0) break;
         {   // stage the record prefetched for this batch
             const float mx = static_cast<float>(pm.x - px0), my = static_cast<float>(pm.y - py0);
             const float Aq = pb0.x, beta = pb0.y, gamma = pb0.z, qhi = pb0.w;
-            sA[t] = make_float4(mx, my, Aq, beta);
-            const float o = pb1.y;
+            const float o = pb1.y, ga = pb1.z;
             float K0 = o, K1 = 0.f, K2 = 0.f, K3 = 0.f;
             if (KIND == 1 && MODE == kQuadricThreshold) {
                 K0 = o * c0; K1 = o * c1; K2 = o * c2; K3 = o * c3;
             }
-            sB[t] = make_float4(gamma, qhi, pb1.x, K0);
-            sC[t] = make_float4(pb1.z, pb1.w, pb2.x, pb2.y);
-            sD[t] = make_float4(K1, K2, K3, __uint_as_float(pi));
-            // coverage of {q <= q_hi}: words (warp, half) hold 4 rows x 8 columns
-            uint32_t cw[8];
+            const float gp = fmaf(1.001f, fmaf(2.2f, 5.9604645e-08f, ga), 4.5e-16f);
+            sA[t] = make_float4(mx, my, Aq, beta);
+            sB[t] = make_float4(gamma, qhi, pb1.x, gp);
+            sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
+            sD[t] = make_float4(-K1, -K2, -K3, 0.f);
+            // coverage of {q <= q_hi}: word w = 8 rows x 4 pairs of warp w's block
+            uint32_t cw[4] = {0u, 0u, 0u, 0u};
             const bool full = MODE != kQuadricThreshold || !(qhi < 3.0e38f) || !(Aq > 0.0f) ||
                               !(gamma > 0.0f) || !(fabsf(beta) < 3.0e38f) || !(fabsf(mx) < 1.0e30f) ||
                               !(fabsf(my) < 1.0e30f);
             if (full || !(qhi >= 0.0f)) {
                 const uint32_t v = full ? 0xFFFFFFFFu : 0u; // everything / never reaches epsilon
 #pragma unroll
-                for (int j = 0; j < 8; ++j) cw[j] = v;
+                for (int j = 0; j < 4; ++j) cw[j] = v;
             } else {
                 const float qpad = qhi * 1.000004f;
                 const float ia = rcp_approx(Aq) * 1.000002f;
 #pragma unroll
-                for (int g = 0; g < 4; ++g) { // rows 4g .. 4g+3 -> words of warps (g>>1)*2 + {0,1}, half g&1
-                    const uint32_t r0 = row_cover(4 * g + 0, mx, my, beta, gamma, qpad, ia);
-                    const uint32_t r1 = row_cover(4 * g + 1, mx, my, beta, gamma, qpad, ia);
-                    const uint32_t r2 = row_cover(4 * g + 2, mx, my, beta, gamma, qpad, ia);
-                    const uint32_t r3 = row_cover(4 * g + 3, mx, my, beta, gamma, qpad, ia);
-                    const uint32_t t01 = __byte_perm(r0, r1, 0x5140), t23 = __byte_perm(r2, r3, 0x5140);
-                    const int wl = (g >> 1) * 4 + (g & 1);     // (warp (g>>1)*2) * 2 + half
-                    cw[wl] = __byte_perm(t01, t23, 0x5410);     // columns 0-7
-                    cw[wl + 2] = __byte_perm(t01, t23, 0x7632); // columns 8-15
+                for (int row = 0; row < 16; ++row) {
+                    const uint32_t m8 = row_pairs(row, mx, my, beta, gamma, qpad, ia);
+                    const int wb = (row >> 3) << 1, sh = (row & 7) << 2;
+                    cw[wb] |= (m8 & 0xFu) << sh;
+                    cw[wb + 1] |= (m8 >> 4) << sh;
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) cover[j][t] = cw[j];
+            for (int j = 0; j < 4; ++j) cover[j][t] = cw[j];
         }
         __syncthreads();
         const int nb = base + kB16;
         if (nb + t < L) { // prefetch the next batch while this one is blended
-            pi = list[nb + t];
+            const uint32_t pi = list[nb + t];
             pm = A.mean2d[pi];
             pb0 = A.bl0[pi];
             pb1 = A.bl1[pi];
@@ -601,31 +712,17 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             const int k0 = g * 32;
             if (k0 >= cnt) break;
             // candidate masks: lane s holds record k0+s's coverage of this warp's
-            // block; the transpose gives lane L's pixels' masks over the 32 records
-            uint32_t w0 = 0u, w1 = 0u;
-            if (k0 + lane < cnt) {
-                w0 = cover[warp * 2][k0 + lane];
-                w1 = cover[warp * 2 + 1][k0 + lane];
-            }
-            if (!__any_sync(0xffffffffu, (w0 | w1) != 0u)) continue;
-            uint32_t m0 = warp_transpose32(w0, tkeep, trot);
-            uint32_t m1 = warp_transpose32(w1, tkeep, trot);
-            if (!(p0.x == p0.x)) m0 = 0u;
-            if (!(p1.x == p1.x)) m1 = 0u;
-            // both pixels' candidates in list order, one of each per step
+            // block; the transpose gives lane L's pair its mask over the 32 records
+            const uint32_t w = k0 + lane < cnt ? cover[warp][k0 + lane] : 0u;
+            if (!__any_sync(0xffffffffu, w != 0u)) continue;
+            uint32_t m = warp_transpose32(w, tkeep, trot);
             const uint32_t rb = s_rec + static_cast<uint32_t>(k0) * 16u;
             const int jb = base + k0;
-            while ((m0 | m1) != 0u) {
-                const bool v0 = m0 != 0u, v1 = m1 != 0u;
-                // (bit 31 forced so an empty mask still yields a valid record slot)
-                const uint32_t j0 = static_cast<uint32_t>(__ffs(m0 | 0x80000000u) - 1);
-                const uint32_t j1 = static_cast<uint32_t>(__ffs(m1 | 0x80000000u) - 1);
-                m0 &= m0 - 1u;
-                m1 &= m1 - 1u;
-                cand_step<KIND, ORDER, MODE, COUNT>(p0, v0, rb + j0 * 16u, yc0, P, jb + static_cast<int>(j0));
-                cand_step<KIND, ORDER, MODE, COUNT>(p1, v1, rb + j1 * 16u, yc1, P, jb + static_cast<int>(j1));
-                if (!(p0.x == p0.x)) m0 = 0u; // finished or flagged
-                if (!(p1.x == p1.x)) m1 = 0u;
+            if (!((f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x)))) m = 0u; // both finished
+            while (m != 0u) {
+                const uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
+                m &= m - 1u;
+                pair_step<KIND, ORDER, MODE, COUNT>(p, rb + j * 16u, yc, P, jb + static_cast<int>(j), m);
             }
         }
     }
@@ -633,24 +730,25 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     unsigned long long ev = 0, bl = 0;
     if (t == 0) s_nflag = 0;
     __syncthreads();
-    auto finish = [&](Px& p, bool inside, int lyp) {
+    auto finish = [&](bool inside, int pxl, bool flagged, float r, float g, float b, float T, uint32_t term,
+                      uint32_t nbl) {
         if (!inside) return;
-        if (p.flagged) { // replayed below
-            s_flag[atomicAdd(&s_nflag, 1u)] = static_cast<uint16_t>(lyp * 16 + lx);
+        if (flagged) { // replayed below
+            s_flag[atomicAdd(&s_nflag, 1u)] = static_cast<uint16_t>(ly * 16 + pxl);
             return;
         }
-        const size_t pix = static_cast<size_t>(py0 + lyp) * W + px0 + lx;
-        A.out_rgb[3 * pix + 0] = p.r;
-        A.out_rgb[3 * pix + 1] = p.g;
-        A.out_rgb[3 * pix + 2] = p.b;
-        A.out_t[pix] = p.T;
+        const size_t pix = static_cast<size_t>(py0 + ly) * W + px0 + pxl;
+        A.out_rgb[3 * pix + 0] = r;
+        A.out_rgb[3 * pix + 1] = g;
+        A.out_rgb[3 * pix + 2] = b;
+        A.out_t[pix] = T;
         if (COUNT) {
-            ev += p.term != 0xffffffffu ? p.term + 1u : static_cast<unsigned>(L);
-            bl += p.nbl;
+            ev += term != 0xffffffffu ? term + 1u : static_cast<unsigned>(L);
+            bl += nbl;
         }
     };
-    finish(p0, in0, ly0);
-    finish(p1, in1, ly0 + 4);
+    finish(in0, lx, p.flag & 1u, f2lo(p.r), f2lo(p.g), f2lo(p.b), f2lo(p.T), p.term0, p.nbl0);
+    finish(in1, lx + 1, p.flag & 2u, f2hi(p.r), f2hi(p.g), f2hi(p.b), f2hi(p.T), p.term1, p.nbl1);
     __syncthreads();
     const int nf = static_cast<int>(s_nflag);
     for (int k = warp; k < nf; k += 4)
