@@ -48,7 +48,7 @@ SOURCES = [
     ("hostmath.cpp", []),
     ("synth.cpp", []),
 ]
-HEADERS = ["common.cuh", "exact_math.cuh", "kernels.h"]
+HEADERS = ["common.cuh", "exact_math.cuh", "kernels.h", "tile_sort.cuh"]
 
 
 def _cmd(src: str, extra: list[str], obj: str) -> list[str]:

@@ -21,7 +21,7 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanPer = 16; // consecutive tiles per thread per round (16K tiles per round)
 
 // One CTA: exclusive scan of the per-tile pair counts into ranges and K3
-// cursors, the total / longest bucket, and the list of buckets > 2048 (sorted
+// cursors, the total / longest bucket, and the list of buckets > kBlendSortCap (sorted
 // outside the blend). Each thread owns 16 consecutive tiles (vector loads and
 // stores), so a 1080p frame (8160 tiles) is one round.
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict__ count, uint2* __restrict__ ranges,
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
 #pragma unroll
             for (int q = 0; q < kScanPer; ++q) {
                 cur[q] = excl;
-                if (v[q] > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
+                if (v[q] > kBlendSortCap) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
                 excl += v[q];
             }
 #pragma unroll
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
                 if (t < n_tiles) {
                     ranges[t] = make_uint2(excl, excl + v[q]);
                     count[t] = excl;
-                    if (v[q] > 2048u) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
+                    if (v[q] > kBlendSortCap) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
                 }
                 excl += v[q];
             }
@@ -109,18 +109,20 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
 // Small buckets (length <= CAP): one CTA per tile over the whole grid.
 template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_small(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
+                                                             const uint32_t* __restrict__ pkey,
                                                              const unsigned long long* __restrict__ key,
                                                              const uint32_t* __restrict__ orig) {
     extern __shared__ uint32_t smem[];
     const uint2 r = ranges[blockIdx.x];
     const int L = static_cast<int>(r.y - r.x);
     if (L <= 1 || L > THREADS * ROUNDS) return;
-    sort_one_tile<THREADS, ROUNDS>(r, pval, key, orig, smem);
+    sort_one_tile<THREADS, ROUNDS>(r, pval, pkey, key, orig, smem);
 }
 
 // Large buckets: grid-stride over the device-built list of long tiles.
 template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
+                                                            const uint32_t* __restrict__ pkey,
                                                             const unsigned long long* __restrict__ key,
                                                             const uint32_t* __restrict__ orig,
                                                             const uint32_t* __restrict__ list, const uint32_t* count,
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
         const uint2 r = ranges[list[q]];
         const int L = static_cast<int>(r.y - r.x);
         if (L <= min_len_exclusive || L > THREADS * ROUNDS) continue;
-        sort_one_tile<THREADS, ROUNDS>(r, pval, key, orig, smem);
+        sort_one_tile<THREADS, ROUNDS>(r, pval, pkey, key, orig, smem);
         __syncthreads();
     }
 }
@@ -153,19 +155,19 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
     if (max_len <= 1 || n_tiles == 0) return true;
     if (max_len > kMaxBucketSorted) return false;
     using S1 = TileSortSmem<128, 16>;
-    k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.key, orig);
+    k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig);
     if (launches) *launches += 1;
-    if (max_len > 2048u) {
+    if (max_len > kBlendSortCap) {
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-        k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
+        k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
+                                                                   &d_ctr->big_tiles, kBlendSortCap, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
@@ -177,17 +179,17 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches) {
     const bool unknown = max_len == 0xffffffffu;
-    if (max_len <= 2048u) return true;
+    if (max_len <= kBlendSortCap) return true;
     if (max_len > kMaxBucketSorted && !unknown) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-    k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
-                                                               &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
+    k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
+                                                               &d_ctr->big_tiles, kBlendSortCap, f.gate, f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.key, orig, f.big_tiles,
+        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }

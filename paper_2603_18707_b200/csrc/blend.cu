@@ -28,6 +28,7 @@ struct BlendArgs {
     const uint2* ranges;
     const uint32_t* pval;
     uint32_t* pval_w;                  // buckets to sort in the prologue (null: presorted)
+    const uint32_t* pkey;              // coarse depth key per bucket entry (K3)
     const unsigned long long* key;     // fp64 depth bits (sort key)
     const uint32_t* orig;              // original splat index (tie-break)
     const double2* mean2d;
@@ -245,7 +246,9 @@ __global__ void k_blend(const BlendArgs A) {
 constexpr int kB16 = 128;
 constexpr float kNaNf = __builtin_nanf("");
 // byte offsets of the record planes a, b, c, d in the staging area
-constexpr uint32_t kOffB = kB16 * 16, kOffC = 2 * kB16 * 16, kOffD = 3 * kB16 * 16;
+// (planes of kB16 + 1 records: slot kB16 is the null record, never accepted)
+constexpr int kRecs = kB16 + 1;
+constexpr uint32_t kOffB = kRecs * 16, kOffC = 2 * kRecs * 16, kOffD = 3 * kRecs * 16;
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
     float4 v;
@@ -270,14 +273,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // Warp-wide 32x32 bit-matrix transpose: lane r holds row r (bit c = element
 // (r, c)); returns column `lane` (bit r = element (r, lane)). Five block-swap
-// steps; keep[s] / rot[s] are the lane's select mask and rotation for step s.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const uint32_t (&keep)[5],
-                                                     const uint32_t (&rot)[5]) {
+// steps; each lane's select mask and rotation per step come from its lane bits.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 #pragma unroll
     for (int s = 0; s < 5; ++s) {
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16 >> s);
-        const uint32_t yr = __funnelshift_l(y, y, rot[s]);
-        x = (x & keep[s]) | (yr & ~keep[s]);
+        const int j = 16 >> s;
+        const uint32_t m = s == 0 ? 0x0000FFFFu : s == 1 ? 0x00FF00FFu : s == 2 ? 0x0F0F0F0Fu : s == 3 ? 0x33333333u
+                                                                                                     : 0x55555555u;
+        const bool up = (lane & j) != 0;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        const uint32_t yr = __funnelshift_l(y, y, up ? 32u - j : static_cast<uint32_t>(j));
+        const uint32_t keep = up ? ~m : m;
+        x = (x & keep) | (yr & ~keep);
     }
     return x;
 }
@@ -369,32 +376,41 @@ struct Pair {
     uint32_t flag;          // bit p: pixel p needs the exact replay
 };
 
-// One record (staged at shared address rec, list position jpos) for both pixels
-// of the pair at row centre yc. m: the pair's remaining candidates (cleared
-// when both pixels are finished).
-template <int KIND, int ORDER, int MODE, bool COUNT>
-__device__ __forceinline__ void pair_step(Pair& p, uint32_t rec, float yc, const FrameParams& P, int jpos,
-                                          uint32_t& m) {
+// One record's fragments for both pixels of a pair: everything that does not
+// depend on the pixels' running state (so two records' fragments can be
+// computed back to back and their latencies overlap).
+struct Frag {
+    float n0, n1;          // -alpha (0 when skipped)
+    float g0, g1;          // g' (0 when skipped)
+    float cr, cg, cb;      // -colour
+    bool skip0, skip1;     // certainly alpha < eps in the reference (or pixel finished)
+    bool amb0, amb1;       // accepted, but the alpha < eps decision is not certified in fp32
+};
+
+// Fragments of the record staged at shared address rec for the pair's pixels
+// (x = their tile-local centres) at row centre yc.
+template <int KIND, int ORDER, int MODE>
+__device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const FrameParams& P) {
     const float4 a = lds128(rec);
     const float4 b = lds128(rec + kOffB);
     const float4 c = lds128(rec + kOffC);
     const float dy = yc - a.y;
     const float mr = fmaf(-a.w, dy, a.x);
     const float cr = b.x * dy * dy;
-    const F2 u = f2sub(p.x, f2b(mr));
+    const F2 u = f2sub(x, f2b(mr));
     const F2 q = f2fma(f2mul(u, f2b(a.z)), u, f2b(cr));
     const float q0 = f2lo(q), q1 = f2hi(q);
-    float n0, n1; // -alpha
-    bool skip0, skip1, amb;
+    Frag f;
     if (MODE == kQuadricThreshold) {
         // the coverage masks are a superset: q > q_hi is a certain skip; q in
         // the certified band [q_lo, q_hi] leaves the reference's alpha < eps
         // undecided in fp32 -> exact replay of the pixel. Accepted fragments
         // have q < q* + Gq < first_root, where the ReLU / piecewise cut-offs
         // are inactive: alpha = min(.999, sum K_j q^j)
-        skip0 = !(q0 <= b.y);
-        skip1 = !(q1 <= b.y);
-        amb = ((q0 >= b.z) & !skip0) | ((q1 >= b.z) & !skip1);
+        f.skip0 = !(q0 <= b.y);
+        f.skip1 = !(q1 <= b.y);
+        f.amb0 = q0 >= b.z;
+        f.amb1 = q1 >= b.z;
         F2 na;
         if (KIND == 0) {
             const F2 ar = f2fma(q, f2b(-0.72134752044448170f), f2b(c.x));
@@ -408,8 +424,8 @@ __device__ __forceinline__ void pair_step(Pair& p, uint32_t rec, float yc, const
             pq = f2fma(pq, q, f2b(d.x));
             na = f2fma(pq, q, f2b(c.x));
         }
-        n0 = fmaxf(-0.999f, f2lo(na));
-        n1 = fmaxf(-0.999f, f2hi(na));
+        f.n0 = fmaxf(-0.999f, f2lo(na));
+        f.n1 = fmaxf(-0.999f, f2hi(na));
     } else {
         // non-monotone kernel: full ReLU / piecewise semantics, guard on alpha
         const KernelF32& kf = P.kf;
@@ -431,17 +447,29 @@ __device__ __forceinline__ void pair_step(Pair& p, uint32_t rec, float yc, const
         const float ga = b.y; // |alpha_fp32 - alpha_ref| bound in this mode
         a0 = fminf(0.999f, a0);
         a1 = fminf(0.999f, a1);
-        skip0 = !(a0 >= P.eps_f - ga);
-        skip1 = !(a1 >= P.eps_f - ga);
-        amb = ((a0 < P.eps_f + ga) & !skip0) | ((a1 < P.eps_f + ga) & !skip1);
-        n0 = -a0;
-        n1 = -a1;
+        f.skip0 = !(a0 >= P.eps_f - ga);
+        f.skip1 = !(a1 >= P.eps_f - ga);
+        f.amb0 = a0 < P.eps_f + ga;
+        f.amb1 = a1 < P.eps_f + ga;
+        f.n0 = -a0;
+        f.n1 = -a1;
     }
-    float g0 = b.w, g1 = b.w;
-    if (skip0) { n0 = 0.0f; g0 = 0.0f; }
-    if (skip1) { n1 = 0.0f; g1 = 0.0f; }
-    F2 na = f2(n0, n1);
-    const F2 gp = f2(g0, g1);
+    f.g0 = f.g1 = b.w;
+    if (f.skip0) { f.n0 = 0.0f; f.g0 = 0.0f; f.amb0 = false; }
+    if (f.skip1) { f.n1 = 0.0f; f.g1 = 0.0f; f.amb1 = false; }
+    f.cr = c.y; f.cg = c.z; f.cb = c.w;
+    return f;
+}
+
+// Blends fragment f (list position jpos) into the pair. When a pixel finishes
+// here, `next` (the following record's fragments, already computed) is
+// cancelled for it; m (the pair's remaining candidates) is cleared when both
+// pixels are finished.
+template <bool COUNT>
+__device__ __forceinline__ void pair_blend(Pair& p, Frag f, int jpos, const FrameParams& P, uint32_t& m,
+                                           Frag* next) {
+    F2 na = f2(f.n0, f.n1);
+    const F2 gp = f2(f.g0, f.g1);
     F2 tt = f2fma(na, p.T, p.T); // T (1 - alpha), one rounding; == T when skipped
     const F2 up = f2fma(p.Up, gp, f2fma(na, p.Up, p.Up));
     F2 lo = f2fma(p.Lo, f2mul(gp, f2b(-1.0f)), f2fma(na, p.Lo, p.Lo));
@@ -449,47 +477,46 @@ __device__ __forceinline__ void pair_step(Pair& p, uint32_t rec, float yc, const
     // its test_t < floor; Lo' >= floor certifies it does not (the common case,
     // no branch); otherwise decide per pixel below.
     const float fl = P.floor_f;
-    if (__builtin_expect(amb | (fminf(f2lo(lo), f2hi(lo)) < fl), 0)) {
-        const F2 hi = up; // < floor: certainly below it
+    if (__builtin_expect((f.amb0 | f.amb1) | (fminf(f2lo(lo), f2hi(lo)) < fl), 0)) {
         float x0 = f2lo(p.x), x1 = f2hi(p.x);
         bool done0 = false, done1 = false;
-        if (!skip0) {
-            const bool amb0 = MODE == kQuadricThreshold ? q0 >= b.z : -n0 < P.eps_f + b.y;
-            if (amb0 || f2lo(lo) < fl) {
-                done0 = true;
-                if (!amb0 && f2lo(hi) < fl) { if (COUNT) p.term0 = static_cast<uint32_t>(jpos); }
-                else p.flag |= 1u;
-            }
+        if (!f.skip0 && (f.amb0 || f2lo(lo) < fl)) {
+            done0 = true;
+            if (!f.amb0 && f2lo(up) < fl) { if (COUNT) p.term0 = static_cast<uint32_t>(jpos); }
+            else p.flag |= 1u;
         }
-        if (!skip1) {
-            const bool amb1 = MODE == kQuadricThreshold ? q1 >= b.z : -n1 < P.eps_f + b.y;
-            if (amb1 || f2hi(lo) < fl) {
-                done1 = true;
-                if (!amb1 && f2hi(hi) < fl) { if (COUNT) p.term1 = static_cast<uint32_t>(jpos); }
-                else p.flag |= 2u;
-            }
+        if (!f.skip1 && (f.amb1 || f2hi(lo) < fl)) {
+            done1 = true;
+            if (!f.amb1 && f2hi(up) < fl) { if (COUNT) p.term1 = static_cast<uint32_t>(jpos); }
+            else p.flag |= 2u;
         }
-        // a finished pixel does not blend this fragment and keeps its T (alpha
-        // = 0 below); a huge Lo keeps it out of this branch from now on
+        // a finished pixel does not blend this fragment (nor the next one) and
+        // keeps its T (alpha = 0 below); a huge Lo keeps it out of this branch
         float l0 = f2lo(lo), l1 = f2hi(lo);
-        if (done0) { n0 = 0.0f; x0 = kNaNf; skip0 = true; l0 = 3.0e38f; }
-        if (done1) { n1 = 0.0f; x1 = kNaNf; skip1 = true; l1 = 3.0e38f; }
+        if (done0) {
+            f.n0 = 0.0f; x0 = kNaNf; f.skip0 = true; l0 = 3.0e38f;
+            if (next) { next->n0 = 0.0f; next->g0 = 0.0f; next->skip0 = true; next->amb0 = false; }
+        }
+        if (done1) {
+            f.n1 = 0.0f; x1 = kNaNf; f.skip1 = true; l1 = 3.0e38f;
+            if (next) { next->n1 = 0.0f; next->g1 = 0.0f; next->skip1 = true; next->amb1 = false; }
+        }
         p.x = f2(x0, x1);
-        na = f2(n0, n1);
+        na = f2(f.n0, f.n1);
         tt = f2fma(na, p.T, p.T);
         lo = f2(l0, l1);
         if (x0 != x0 && x1 != x1) m = 0u; // both pixels finished
     }
     const F2 w = f2mul(na, p.T); // -alpha T
-    p.r = f2fma(w, f2b(c.y), p.r);
-    p.g = f2fma(w, f2b(c.z), p.g);
-    p.b = f2fma(w, f2b(c.w), p.b);
+    p.r = f2fma(w, f2b(f.cr), p.r);
+    p.g = f2fma(w, f2b(f.cg), p.g);
+    p.b = f2fma(w, f2b(f.cb), p.b);
     p.T = tt;
     p.Up = up;
     p.Lo = lo;
     if (COUNT) {
-        p.nbl0 += skip0 ? 0u : 1u;
-        p.nbl1 += skip1 ? 0u : 1u;
+        p.nbl0 += f.skip0 ? 0u : 1u;
+        p.nbl1 += f.skip1 ? 0u : 1u;
     }
 }
 
@@ -592,20 +619,22 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 
 template <int KIND, int ORDER, int MODE, bool COUNT>
 __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
-    using SortSm = TileSortSmem<128, 16>;
+    using SortSm = TileSortSmem<128, kBlendSortCap / 128>;
+    static_assert(SortSm::CAP == static_cast<int>(kBlendSortCap), "prologue sort capacity");
     // Shared memory: the bucket sort's workspace; the sorted list starts at word
     // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
     // overlay the sort's dead arrays below it.
     __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];
-    static_assert(4 * kB16 * 16 + 4 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
+    static_assert(4 * kRecs * 16 + 4 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
     float4* sA = reinterpret_cast<float4*>(S);
-    float4* sB = sA + kB16;
-    float4* sC = sA + 2 * kB16;
-    float4* sD = sA + 3 * kB16;
-    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kB16); // [warp][record]
+    float4* sB = sA + kRecs;
+    float4* sC = sA + 2 * kRecs;
+    float4* sD = sA + 3 * kRecs;
+    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kRecs); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
+    const uint32_t s_null = s_rec + kB16 * 16u;
 
     if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
     const FrameParams& P = A.P;
@@ -629,23 +658,13 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     p.nbl0 = p.nbl1 = 0u;
     p.flag = 0u;
     const float c0 = P.kf.c[0], c1 = P.kf.c[1], c2 = P.kf.c[2], c3 = P.kf.c[3];
-    uint32_t tkeep[5], trot[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int j = 16 >> k;
-        const uint32_t m = k == 0 ? 0x0000FFFFu : k == 1 ? 0x00FF00FFu : k == 2 ? 0x0F0F0F0Fu : k == 3 ? 0x33333333u
-                                                                                                     : 0x55555555u;
-        tkeep[k] = (lane & j) ? ~m : m;
-        trot[k] = (lane & j) ? 32u - j : static_cast<uint32_t>(j);
-    }
-
     const uint2 range = A.ranges[tile];
     const int L = static_cast<int>(range.y - range.x);
     // the tile's list in (depth, index) order: sorted here for buckets that fit
     // one CTA, presorted in global memory otherwise
     const uint32_t* list = A.pval + range.x;
     if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, 16, false>(range, A.pval_w, A.key, A.orig, S);
+        list = sort_one_tile<128, kBlendSortCap / 128, false>(range, A.pval_w, A.pkey, A.key, A.orig, S);
         __syncthreads();
     }
     double2 pm = make_double2(0.0, 0.0);
@@ -674,6 +693,12 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             sB[t] = make_float4(gamma, qhi, pb1.x, gp);
             sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
             sD[t] = make_float4(-K1, -K2, -K3, 0.f);
+            if (t == 0) { // null record: q = dy^2 > q_hi = -1 (alpha mode: alpha 0 < eps + 1)
+                sA[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
+                sB[kB16] = make_float4(1.f, -1.f, 3.0e38f, 0.f);
+                sC[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
+                sD[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
             // coverage of {q <= q_hi}: word w = 8 rows x 4 pairs of warp w's block
             uint32_t cw[4] = {0u, 0u, 0u, 0u};
             const bool full = MODE != kQuadricThreshold || !(qhi < 3.0e38f) || !(Aq > 0.0f) ||
@@ -715,14 +740,23 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             // block; the transpose gives lane L's pair its mask over the 32 records
             const uint32_t w = k0 + lane < cnt ? cover[warp][k0 + lane] : 0u;
             if (!__any_sync(0xffffffffu, w != 0u)) continue;
-            uint32_t m = warp_transpose32(w, tkeep, trot);
+            uint32_t m = warp_transpose32(w, lane);
             const uint32_t rb = s_rec + static_cast<uint32_t>(k0) * 16u;
             const int jb = base + k0;
             if (!((f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x)))) m = 0u; // both finished
+            // two candidates per iteration (the second one the null record
+            // when only one is left): both records' fragments first, so their
+            // loads and arithmetic overlap, then the two blends in list order
             while (m != 0u) {
-                const uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
+                const uint32_t j1 = static_cast<uint32_t>(__ffs(m) - 1);
                 m &= m - 1u;
-                pair_step<KIND, ORDER, MODE, COUNT>(p, rb + j * 16u, yc, P, jb + static_cast<int>(j), m);
+                const uint32_t j2 = m ? static_cast<uint32_t>(__ffs(m) - 1) : j1;
+                const uint32_t r2 = m ? rb + j2 * 16u : s_null;
+                m &= m - 1u;
+                const Frag f1 = pair_frag<KIND, ORDER, MODE>(p.x, rb + j1 * 16u, yc, P);
+                Frag f2_ = pair_frag<KIND, ORDER, MODE>(p.x, r2, yc, P);
+                pair_blend<COUNT>(p, f1, jb + static_cast<int>(j1), P, m, &f2_);
+                pair_blend<COUNT>(p, f2_, jb + static_cast<int>(j2), P, m, nullptr);
             }
         }
     }
@@ -798,6 +832,7 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     a.ranges = f.ranges;
     a.pval = pair_vals;
     a.pval_w = sort_in_place;
+    a.pkey = f.pkey;
     a.key = f.key;
     a.orig = orig;
     a.mean2d = f.mean2d;

@@ -395,12 +395,12 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
         f.gate = c->d_ctr;
         f.pair_cap = static_cast<unsigned long long>(c->p_cap);
-        launch_duplicate_buckets(f, P, n, strm);
+        launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
         launches += n > 0;
         record(c, 4);
-        // buckets > 2048 (sorted outside the blend): launched when the last
-        // frame had any; a frame that has them unannounced is re-run
-        const bool long_sorts = c->last_max_len > 2048u;
+        // buckets > kBlendSortCap (sorted outside the blend): launched when the
+        // last frame had any; a frame that has them unannounced is re-run
+        const bool long_sorts = c->last_max_len > kBlendSortCap;
         if (long_sorts) launch_tile_sort_long(f, s->dev.orig, 0xffffffffu, c->d_ctr, strm, &launches);
         record(c, 5);
         BlendOut out{req.d_rgb, req.d_t};
@@ -415,7 +415,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         if ((st = check_counters()) != PS_OK) return st;
         c->last_max_len = res.ctr.max_tile_len;
         if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
-            (!long_sorts && res.ctr.max_tile_len > 2048u)) {
+            (!long_sorts && res.ctr.max_tile_len > kBlendSortCap)) {
             FrameRequest sized = req;
             sized.no_speculation = true;
             return run_frame(c, s, cam, cfg_in, sized, res);
@@ -441,7 +441,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     uint32_t* sort_in_blend = nullptr;
     if (res.ctr.max_tile_len <= kMaxBucketSorted) {
         // K3: scatter splat indices into per-tile buckets
-        launch_duplicate_buckets(f, P, n, strm);
+        launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
         launches += n > 0;
         record(c, 4);
         // K4: exact (depth, index) order inside every bucket — long buckets

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "exact_math.cuh"
 #include "kernels.h"
+#include "tile_sort.cuh"
 
 namespace ps {
 
@@ -587,16 +588,22 @@ __global__ void __launch_bounds__(256) k_duplicate(FrameDev f, FrameParams P, co
 // exact key.
 // Rects larger than 8x8 tiles (rare): exact tests, direct global atomics.
 // Out of line with scalar arguments so the common path keeps few registers.
-__device__ __noinline__ void duplicate_big(uint32_t* __restrict__ pval, uint32_t* __restrict__ tile_count,
+__device__ __noinline__ void duplicate_big(uint32_t* __restrict__ pval, uint32_t* __restrict__ pkey, uint32_t k32,
+                                           uint32_t* __restrict__ tile_count,
                                            double2 mm, double2 ab, double2 cq, int ts, int tiles_x, uint32_t i,
                                            int r0, int r1, int r2, int r3) {
     const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
     for (int ty = r1; ty <= r3; ++ty)
         for (int tx = r0; tx <= r2; ++tx)
-            if (tight_test_fast(t, tx, ty, ts)) pval[atomicAdd(&tile_count[ty * tiles_x + tx], 1u)] = i;
+            if (tight_test_fast(t, tx, ty, ts)) {
+                const uint32_t o = atomicAdd(&tile_count[ty * tiles_x + tx], 1u);
+                pval[o] = i;
+                pkey[o] = k32;
+            }
 }
 
-__global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n) {
+__global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n,
+                                                               const DevCounters* __restrict__ ctr) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
     if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
@@ -605,14 +612,16 @@ __global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameP
     int r[4] = {0, 0, -1, -1};
     unsigned long long m0 = 0ull;
     bool small = false;
+    uint32_t k32 = 0u; // coarse depth key stored next to every bucket entry (tile_sort.cuh)
     if (active) {
+        k32 = coarse_key(f.key[i], ~ctr->key_min, ctr->key_max);
         const ushort4 rc = f.rect[i];
         r[0] = rc.x; r[1] = rc.y; r[2] = rc.z; r[3] = rc.w;
         if (rect_is_small(r)) {
             small = true;
             m0 = f.tmask[i];
         } else { // big rect: exact tests, direct atomics (rare)
-            duplicate_big(f.pval, f.tile_count, f.mean2d[i], f.conic_ab[i], f.conic_cq[i], P.cfg.tile_size,
+            duplicate_big(f.pval, f.pkey, k32, f.tile_count, f.mean2d[i], f.conic_ab[i], f.conic_cq[i], P.cfg.tile_size,
                           P.tiles_x, static_cast<uint32_t>(i), r[0], r[1], r[2], r[3]);
         }
     }
@@ -634,14 +643,18 @@ __global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameP
         while (m) {
             const int b = __ffsll(static_cast<long long>(m)) - 1;
             m &= m - 1;
-            f.pval[atomicAdd(&win[rect_bit_win(r, b, W)], 1u)] = static_cast<uint32_t>(i);
+            const uint32_t o = atomicAdd(&win[rect_bit_win(r, b, W)], 1u);
+            f.pval[o] = static_cast<uint32_t>(i);
+            f.pkey[o] = k32;
         }
     } else if (small) {
         unsigned long long m = m0;
         while (m) {
             const int b = __ffsll(static_cast<long long>(m)) - 1;
             m &= m - 1;
-            f.pval[atomicAdd(&f.tile_count[rect_bit_tile(r, b, P.tiles_x)], 1u)] = static_cast<uint32_t>(i);
+            const uint32_t o = atomicAdd(&f.tile_count[rect_bit_tile(r, b, P.tiles_x)], 1u);
+            f.pval[o] = static_cast<uint32_t>(i);
+            f.pkey[o] = k32;
         }
     }
 }
@@ -781,10 +794,11 @@ void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* o
     k_duplicate<<<blocks, 256, 0, st>>>(f, P, order, n);
 }
 
-void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st) {
+void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
+                              cudaStream_t st) {
     if (n == 0) return;
     const int blocks = static_cast<int>((n + 255) / 256);
-    k_duplicate_buckets<<<blocks, 256, 0, st>>>(f, P, n);
+    k_duplicate_buckets<<<blocks, 256, 0, st>>>(f, P, n, ctr);
 }
 
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,

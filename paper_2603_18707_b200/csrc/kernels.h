@@ -11,6 +11,9 @@ namespace ps {
 // Longest per-tile bucket sorted in shared memory (binning.cu); longer tiles
 // take the global radix-sort path.
 constexpr uint32_t kMaxBucketSorted = 12288u;
+// Longest bucket the blend kernel sorts in its prologue (16x16 tiles); longer
+// ones are sorted by the list kernels (binning.cu) before the blend.
+constexpr uint32_t kBlendSortCap = 2048u;
 
 // exact_kernels.cu (-fmad=false)
 void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
@@ -19,7 +22,9 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
 void launch_scene_cov(const SceneDev& s, cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
                       cudaStream_t st);
-void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, cudaStream_t st);
+// K3 also stores each entry's coarse depth key (tile_sort.cuh coarse_key) in f.pkey
+void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
+                              cudaStream_t st);
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
                    float* out_t, bool count_work, int sm_count, cudaStream_t st);
 

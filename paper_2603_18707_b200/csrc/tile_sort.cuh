@@ -10,24 +10,37 @@ namespace ps {
 
 // Exact per-tile order (the reference comparator, raster.cpp:172-175:
 // fp64 depth, then splat index; positive fp64 depths order like their bits):
-//  1. 32-bit key = (depth bits - tile minimum) scaled to the tile's own depth
-//     span (an order-preserving map); one counting-sort pass on its top
-//     log2(BINS) bits (shared-memory histogram + atomic cursors, so the order
-//     inside a bin is arbitrary);
+//  0. K3 stored next to every bucket entry a 32-bit coarse depth key
+//     (pkey: the frame-global, order-preserving (bits - min) >> shift; see
+//     coarse_key), read here coalesced instead of gathering the 64-bit keys;
+//  1. 32-bit key = (coarse key - tile minimum) scaled to the tile's own
+//     span (order-preserving, injective on coarse keys); one counting-sort
+//     pass on its top log2(BINS) bits (shared-memory histogram + atomic
+//     cursors, so the order inside a bin is arbitrary);
 //  2. every item of a bin holding n > 1 items gets its rank inside the bin by
 //     counting the bin's items that precede it in (32-bit key, full depth bits,
-//     original index) — n compares per item, all items in parallel. A bin of
+//     original index) — n compares per item, all items in parallel; the
+//     64-bit depths are gathered only for equal 32-bit keys. A bin of
 //     more than kMaxRun items (a degenerate depth cluster) switches the CTA to
 //     a bitonic sort on the full key, which is exact for any input.
 constexpr int kMaxRun = 256;
 
 constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2_c(v >> 1); }
 
+// Frame-global coarse key of a visible splat's depth bits: order-preserving
+// (monotone non-decreasing), from the frame's key range [kmin, kmax].
+__device__ __forceinline__ uint32_t coarse_key(unsigned long long k, unsigned long long kmin,
+                                               unsigned long long kmax) {
+    const unsigned long long span = kmax - kmin;
+    const int nb = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+    return static_cast<uint32_t>((k - kmin) >> (nb > 32 ? nb - 32 : 0));
+}
+
 template <int THREADS, int ROUNDS>
 struct TileSortSmem {
     static constexpr int CAP = THREADS * ROUNDS;
     static constexpr int WARPS = THREADS / 32;
-    static constexpr int BINS = CAP >= 8192 ? 4096 : 2048;
+    static constexpr int BINS = CAP >= 8192 ? 4096 : CAP >= 2048 ? 2048 : 1024;
     static constexpr int BIN_SHIFT = 32 - ilog2_c(BINS);
     // vin [CAP] u32 | nk [CAP] u32 | perm [CAP] u16 | dest [CAP] u16 | hist [BINS] -> sorted list [CAP]
     static constexpr int LIST = 3 * CAP; // word offset of the sorted list
@@ -39,6 +52,7 @@ struct TileSortSmem {
 // writes it to pval[r.x, r.y). The caller synchronises before reading it.
 template <int THREADS, int ROUNDS, bool WRITEBACK = true>
 __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __restrict__ pval,
+                                                   const uint32_t* __restrict__ pkey,
                                                    const unsigned long long* __restrict__ key,
                                                    const uint32_t* __restrict__ orig, uint32_t* smem) {
     using S = TileSortSmem<THREADS, ROUNDS>;
@@ -50,17 +64,17 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     uint16_t* perm = reinterpret_cast<uint16_t*>(smem + 2 * CAP);      // bin-sorted position -> slot
     uint16_t* dest = perm + CAP;                                       // bin-sorted position -> final
     uint32_t* hist = smem + S::LIST;                                  // counts -> cursors -> list
-    __shared__ unsigned long long red_min[WARPS], red_max[WARPS];
+    __shared__ uint32_t red_min[WARPS], red_max[WARPS];
     __shared__ uint32_t wsum[WARPS];
     __shared__ int need_bitonic;
 
     const int L = static_cast<int>(r.y - r.x);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    unsigned long long lo = ~0ull, hi = 0ull;
+    uint32_t lo = 0xffffffffu, hi = 0u;
     for (int j = t; j < L; j += THREADS) {
-        const uint32_t v = pval[r.x + j];
-        const unsigned long long k = key[v];
-        vin[j] = v;
+        const uint32_t k = pkey[r.x + j];
+        vin[j] = pval[r.x + j];
+        nk[j] = k;
         lo = min(lo, k);
         hi = max(hi, k);
     }
@@ -76,11 +90,10 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     lo = red_min[0]; hi = red_max[0];
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) { lo = min(lo, red_min[w]); hi = max(hi, red_max[w]); }
-    const unsigned long long span = hi - lo;
-    const int nbits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+    const uint32_t span = hi - lo;
+    const int sh = span ? __clz(static_cast<int>(span)) : 0; // (k - lo) << sh spans the full 32 bits
     for (int j = t; j < L; j += THREADS) {
-        const unsigned long long k = key[vin[j]] - lo;
-        const uint32_t x = nbits > 32 ? static_cast<uint32_t>(k >> (nbits - 32)) : static_cast<uint32_t>(k << (32 - nbits));
+        const uint32_t x = (nk[j] - lo) << sh;
         nk[j] = x;
         atomicAdd(&hist[x >> SH], 1u);
     }

@@ -1,0 +1,49 @@
+"""Aggregates an ncu source export (tools/ncu_kernel.sh) of k_blend16 into
+regions (sort / staging / transpose / walk / replay) by source line ranges."""
+import csv
+import re
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+src = open(sys.argv[2] if len(sys.argv) > 2 else "paper_2603_18707_b200/csrc/blend.cu").read().splitlines()
+
+
+def find(pat, start=0):
+    for i in range(start, len(src)):
+        if re.search(pat, src[i]):
+            return i + 1
+    raise KeyError(pat)
+
+
+k = find(r"__global__ void __launch_bounds__\(128, 6\) k_blend16")
+ranges = {
+    "walk": (find(r"__device__ __forceinline__ void pair_step"), find(r"^// alpha of \(pixel")),
+    "stage+cover": (find(r"stage the record prefetched", k), find(r"prefetch the next batch", k)),
+    "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Shared-memory record")),
+    "transpose": (find(r"warp_transpose32\(uint32_t x"), find(r"^// ---- packed fp32 pairs")),
+    "group loop": (find(r"for \(int g = 0; g < kB16 / 32", k), find(r"unsigned long long ev = 0, bl = 0;", k)),
+    "replay": (find(r"^// alpha of \(pixel"), find(r"^template <int KIND, int ORDER, int MODE, bool COUNT>", k - 3)),
+}
+hdr = next(r for r in rows if r and r[0] == "Line No")
+si, ii = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
+cur, agg = None, {}
+for r in rows:
+    if r and r[0] == "File Path":
+        cur = r[1].split("/")[-1]
+        continue
+    if len(r) > ii and r[0] not in ("", "Line No", "Function Name") and r[2] == "-":
+        ln = int(r[0])
+        if cur == "blend.cu":
+            reg = next((n for n, (a, b) in ranges.items() if a <= ln < b), "kernel body")
+        elif cur.startswith("tile_sort"):
+            reg = "sort"
+        else:
+            reg = "other:" + cur
+        a = agg.setdefault(reg, [0, 0])
+        a[0] += int(r[si] or 0)
+        a[1] += int(r[ii] or 0)
+ts = sum(a[0] for a in agg.values()) or 1
+ti = sum(a[1] for a in agg.values()) or 1
+print(f"total: {ti / 1e6:.1f}M warp instructions, {ts} stall samples")
+for n, (s_, i_) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{n:34s} instr {i_ / 1e6:6.1f}M ({100 * i_ / ti:4.1f}%)  stalls {100 * s_ / ts:5.1f}%")
