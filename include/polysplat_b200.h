@@ -238,6 +238,42 @@ int ps_tile_lists(ps_ctx* ctx, const ps_scene* scene, const ps_camera* cam, cons
                   int64_t capacity, uint32_t* tile_offsets, uint32_t* splat_index,
                   int64_t* n_pairs, ps_counters* counters);
 
+/* ---------------------------------------------------------------- image metrics
+ * Replaces composite / psnr / ssim / max_abs_diff (metrics.hpp:18-30,
+ * metrics.cpp:13-134) on the device. Both framebuffers are composited against
+ * bg[3] (rgb + T * bg), then: psnr_db (peak 1, MSE over all channel values;
+ * +inf for identical images), ssim (11x11 Gaussian window sigma 1.5, valid
+ * mode, mean over channels; ssim_valid = 0 and ssim = 0 when the image is
+ * smaller than 11x11, where the reference throws TooSmall) and max_abs_diff.
+ * Per-pixel terms are computed in fp64 in the reference's operation order; the
+ * sums over pixels are reduced in parallel (relative differences ~1e-15).
+ * dtype: PS_DTYPE_F32 (framebuffers as ps_render writes them) or PS_DTYPE_F64
+ * (the reference's Framebuffer). Buffers in memspace. */
+enum { PS_DTYPE_F32 = 0, PS_DTYPE_F64 = 1 };
+typedef struct ps_image_metrics {
+    double psnr_db;
+    double ssim;
+    double max_abs_diff;
+    int32_t ssim_valid;
+    int32_t reserved;
+} ps_image_metrics;
+int ps_image_metrics_compute(ps_ctx* ctx, int width, int height, const void* rgb_a, const void* t_a,
+                             const void* rgb_b, const void* t_b, int dtype, int memspace, const double* bg,
+                             ps_image_metrics* out);
+
+/* compare (metrics.cpp:138-157): renders cfg_a (the reference side) and cfg_b
+ * of one scene and camera on the device and compares them with
+ * ps_image_metrics_compute; counters_a / counters_b and pair_ratio =
+ * pairs_b / pairs_a (0 when pairs_a == 0) as in CompareReport. */
+typedef struct ps_compare_report {
+    ps_image_metrics metrics;
+    ps_counters counters_a;
+    ps_counters counters_b;
+    double pair_ratio;
+} ps_compare_report;
+int ps_compare(ps_ctx* ctx, const ps_scene* scene, const ps_camera* cam, const ps_config* cfg_a,
+               const ps_config* cfg_b, const double* bg, ps_compare_report* out);
+
 /* ---------------------------------------------------------------- kernel math
  * Host implementations of the exact fp64 math the device preprocess uses
  * (same source, compiled for host). Mirror kernel.cpp. */

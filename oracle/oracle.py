@@ -220,7 +220,7 @@ class Reference(_Lib):
                                     C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.ref_tile_rect.restype = C.c_int
         L.ref_compare_images.argtypes = [C.c_int, C.c_int] + [C.POINTER(C.c_double)] * 5 + [
-            C.POINTER(C.c_double), C.POINTER(C.c_double)]
+            C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_compare_images.restype = C.c_int
         L.ref_resolve_thread_count.argtypes = [C.c_int]
         L.ref_resolve_thread_count.restype = C.c_int
@@ -250,12 +250,14 @@ class Reference(_Lib):
         ok = self.lib.ref_tile_rect(mx, my, dptr(cv), radius, tile_size, width, height, r)
         return tuple(r) if ok else None
 
-    def compare_images(self, rgb_a, t_a, rgb_b, t_b, bg=(1.0, 1.0, 1.0)):
+    def compare_images(self, rgb_a, t_a, rgb_b, t_b, bg=(1.0, 1.0, 1.0), with_ssim=False):
+        """composite + psnr / max_abs_diff (+ ssim) of the reference (metrics.cpp:13-134)."""
         h, w = t_a.shape
         arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (rgb_a, t_a, rgb_b, t_b, bg)]
-        p, m = C.c_double(0), C.c_double(0)
-        self._call("compare_images", w, h, *[dptr(a) for a in arrs], C.byref(p), C.byref(m))
-        return p.value, m.value
+        p, m, s = C.c_double(0), C.c_double(0), C.c_double(0)
+        self._call("compare_images", w, h, *[dptr(a) for a in arrs], C.byref(p), C.byref(m),
+                   C.byref(s) if with_ssim else None)
+        return (p.value, m.value, s.value) if with_ssim else (p.value, m.value)
 
     def resolve_thread_count(self, requested: int = 0) -> int:
         return self.lib.ref_resolve_thread_count(requested)

@@ -361,9 +361,9 @@ double ref_min_quadric_over_box(const double conic[3], double mx, double my, con
                                 PixelBox{box[0], box[1], box[2], box[3]});
 }
 
-// composite + psnr / max_abs_diff (metrics.cpp:13-52), background (bg[3])
+// composite + psnr / max_abs_diff / ssim (metrics.cpp:13-134), background (bg[3]); ssim_out may be NULL
 int ref_compare_images(int w, int h, const double* rgb_a, const double* t_a, const double* rgb_b,
-                       const double* t_b, const double* bg, double* psnr_db, double* max_abs) {
+                       const double* t_b, const double* bg, double* psnr_db, double* max_abs, double* ssim_out) {
     return guarded([&]() -> int {
         Framebuffer a(w, h), b(w, h);
         std::memcpy(a.rgb.data(), rgb_a, a.rgb.size() * sizeof(double));
@@ -374,6 +374,7 @@ int ref_compare_images(int w, int h, const double* rgb_a, const double* t_a, con
         Image ia = composite(a, background), ib = composite(b, background);
         *psnr_db = psnr(ia, ib);
         *max_abs = max_abs_diff(ia, ib);
+        if (ssim_out) *ssim_out = ssim(ia, ib); // throws TooSmall below 11x11
         return PS_OK;
     });
 }

@@ -24,7 +24,7 @@ EXPORTS = (
     "ps_prepare", "ps_tile_lists", "ps_make_polynomial_kernel", "ps_make_exponential_kernel",
     "ps_first_positive_root", "ps_culling_radius", "ps_eval_kernel", "ps_validate_config",
     "ps_validate_camera", "ps_default_config", "ps_synth_scene", "ps_synth_scene_soa",
-    "ps_orbit_cameras",
+    "ps_orbit_cameras", "ps_image_metrics_compute", "ps_compare",
 )
 
 _lib = None
@@ -58,6 +58,9 @@ def _declare(L) -> None:
         "ps_count_pairs": (C.c_int, [vp, vp, cam_p, cfg_p, ctr_p]),
         "ps_prepare": (C.c_int, [vp, vp, cam_p, cfg_p, i64, P(abi.ps_prepared), P(i64), ctr_p]),
         "ps_tile_lists": (C.c_int, [vp, vp, cam_p, cfg_p, i64, P(C.c_uint32), P(C.c_uint32), P(i64), ctr_p]),
+        "ps_image_metrics_compute": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, dp,
+                                              P(abi.ps_image_metrics)]),
+        "ps_compare": (C.c_int, [vp, vp, cam_p, cfg_p, cfg_p, dp, P(abi.ps_compare_report)]),
         "ps_make_polynomial_kernel": (C.c_int, [C.c_int, dp, C.c_int, P(abi.ps_kernel)]),
         "ps_make_exponential_kernel": (abi.ps_kernel, []),
         "ps_first_positive_root": (C.c_int, [dp, C.c_int, dp]),

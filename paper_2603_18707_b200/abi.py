@@ -97,6 +97,30 @@ class ps_counters(C.Structure):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
+class ps_image_metrics(C.Structure):
+    """metrics.hpp:18-30 results (ps_image_metrics_compute)."""
+    _fields_ = [
+        ("psnr_db", C.c_double),
+        ("ssim", C.c_double),
+        ("max_abs_diff", C.c_double),
+        ("ssim_valid", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class ps_compare_report(C.Structure):
+    """CompareReport (metrics.hpp:32-38)."""
+    _fields_ = [
+        ("metrics", ps_image_metrics),
+        ("counters_a", ps_counters),
+        ("counters_b", ps_counters),
+        ("pair_ratio", C.c_double),
+    ]
+
+
+PS_DTYPE_F32, PS_DTYPE_F64 = 0, 1
+
+
 class ps_stats(C.Structure):
     _fields_ = [
         ("visible", C.c_uint64),

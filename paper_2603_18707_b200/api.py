@@ -508,6 +508,37 @@ class Rasterizer:
             if tmp:
                 ds.close()
 
+    # -- quality metrics (metrics.hpp:18-38)
+    def image_metrics(self, a: "Framebuffer", b: "Framebuffer", background=(1.0, 1.0, 1.0)) -> "ImageMetrics":
+        """composite + psnr / ssim / max_abs_diff of two host framebuffers, on the device."""
+        if (a.width, a.height) != (b.width, b.height):
+            raise Error("image dimensions differ")  # DimensionMismatch (metrics.cpp:28-31)
+        f64 = a.rgb.dtype == np.float64 or b.rgb.dtype == np.float64
+        dt = np.float64 if f64 else np.float32
+        arrs = [np.ascontiguousarray(x, dtype=dt) for x in (a.rgb, a.transmittance, b.rgb, b.transmittance)]
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        out = abi.ps_image_metrics()
+        _check(lib().ps_image_metrics_compute(self.handle, a.width, a.height, *[x.ctypes.data for x in arrs],
+                                              abi.PS_DTYPE_F64 if f64 else abi.PS_DTYPE_F32, abi.PS_MEM_HOST,
+                                              abi.dptr(bg), C.byref(out)), self.handle)
+        return ImageMetrics.from_struct(out)
+
+    def compare(self, scene, cam: Camera, cfg_a: RasterConfig, cfg_b: RasterConfig,
+                background=(1.0, 1.0, 1.0)) -> "CompareReport":
+        """polysplat::compare (metrics.cpp:138-157): renders both configs on the device and compares."""
+        ds, tmp = self._scene(scene)
+        try:
+            c, ga, gb = cam.to_struct(), cfg_a.to_struct(), cfg_b.to_struct()
+            bg = np.ascontiguousarray(background, dtype=np.float64)
+            out = abi.ps_compare_report()
+            _check(lib().ps_compare(self.handle, ds.handle, C.byref(c), C.byref(ga), C.byref(gb), abi.dptr(bg),
+                                    C.byref(out)), self.handle)
+            return CompareReport(ImageMetrics.from_struct(out.metrics), PerfCounters.from_struct(out.counters_a),
+                                 PerfCounters.from_struct(out.counters_b), float(out.pair_ratio))
+        finally:
+            if tmp:
+                ds.close()
+
     # -- instrumentation
     def set_timing(self, on: bool = True) -> None:
         _check(lib().ps_ctx_set_timing(self.handle, 1 if on else 0), self.handle)
@@ -548,3 +579,95 @@ def prepare_splats(splats, cam: Camera, cfg: RasterConfig) -> Prepared:
 
 def device_count() -> int:
     return lib().ps_device_count()
+
+
+# ---------------------------------------------------------------- metrics / ablation (metrics.hpp, main.cpp)
+@dataclass
+class ImageMetrics:
+    """psnr / ssim / max_abs_diff of two composited images (metrics.hpp:18-30).
+    ssim is None where the reference throws TooSmall (images under 11x11)."""
+    psnr_db: float
+    ssim: Optional[float]
+    max_abs_diff: float
+
+    @staticmethod
+    def from_struct(m: abi.ps_image_metrics) -> "ImageMetrics":
+        return ImageMetrics(float(m.psnr_db), float(m.ssim) if m.ssim_valid else None, float(m.max_abs_diff))
+
+
+@dataclass
+class CompareReport:
+    """CompareReport (metrics.hpp:32-38)."""
+    metrics: ImageMetrics
+    counters_a: PerfCounters
+    counters_b: PerfCounters
+    pair_ratio: float
+
+    @property
+    def psnr_db(self) -> float:
+        return self.metrics.psnr_db
+
+    @property
+    def ssim(self) -> Optional[float]:
+        return self.metrics.ssim
+
+    @property
+    def max_abs_diff(self) -> float:
+        return self.metrics.max_abs_diff
+
+
+def _fmt17(v: float) -> str:
+    """metrics.cpp fmt17: %.17g, with inf / -inf spelled out."""
+    if math.isinf(v):
+        return "inf" if v > 0 else "-inf"
+    return "%.17g" % v
+
+
+def csv_header() -> str:
+    """metrics.cpp csv_header."""
+    return "label_a,label_b,psnr_db,ssim,max_abs_diff,pairs_a,pairs_b,pair_ratio\n"
+
+
+def csv_row(label_a: str, label_b: str, r: CompareReport) -> str:
+    """metrics.cpp csv_row (values round-trip exactly)."""
+    return (f"{label_a},{label_b},{_fmt17(r.psnr_db)},{_fmt17(r.ssim if r.ssim is not None else 0.0)},"
+            f"{_fmt17(r.max_abs_diff)},{r.counters_a.tile_pairs_after_tight_test},"
+            f"{r.counters_b.tile_pairs_after_tight_test},{_fmt17(r.pair_ratio)}\n")
+
+
+# The reference CLI's ablation cells (tools/main.cpp:315-323): kernel x culling,
+# each compared against exp / StopThePop.
+ABLATION_CELLS = (
+    ("exp/stp", "exp", CullingMode.StopThePop),
+    ("poly1/stp", "poly1", CullingMode.StopThePop),
+    ("poly1/zero", "poly1", CullingMode.ZeroCrossing),
+    ("poly1/opacity", "poly1", CullingMode.OpacityAware),
+    ("poly2p/opacity", "poly2p", CullingMode.OpacityAware),
+    ("poly3/stp", "poly3", CullingMode.StopThePop),
+    ("poly3/opacity", "poly3", CullingMode.OpacityAware),
+)
+
+
+def ablation_grid(rasterizer: "Rasterizer", scene, cam: Camera, base: Optional[RasterConfig] = None,
+                  background=(1.0, 1.0, 1.0), cells=ABLATION_CELLS):
+    """The reference's ablation grid (tools/main.cpp:300-345) on the device:
+    every cell compared against exp / StopThePop with the fitted kernels.
+    Returns (reports by label, csv text in the reference's format)."""
+    base = base or RasterConfig()
+    ds, tmp = rasterizer._scene(scene)
+    try:
+        def cfg(kname, mode):
+            return RasterConfig(tile_size=base.tile_size, epsilon=base.epsilon,
+                                transmittance_floor=base.transmittance_floor, culling_mode=mode,
+                                kernel=fitted_kernel(kname), v_dilation=base.v_dilation,
+                                sh_degree=base.sh_degree, clamp_before_blend=base.clamp_before_blend)
+        ref = cfg("exp", CullingMode.StopThePop)
+        reports, csv = {}, csv_header()
+        for label, kname, mode in cells:
+            r = rasterizer.compare(ds, cam, ref, cfg(kname, mode), background)
+            reports[label] = r
+            csv += csv_row("exp/stp", label, r)
+        return reports, csv
+    finally:
+        if tmp:
+            ds.close()

@@ -44,6 +44,7 @@ SOURCES = [
     ("sort.cu", []),
     ("binning.cu", []),
     ("utils.cu", []),
+    ("metrics.cu", []),
     ("context.cu", []),
     ("hostmath.cpp", []),
     ("synth.cpp", []),

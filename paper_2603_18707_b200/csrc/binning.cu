@@ -111,8 +111,10 @@ template <int THREADS, int ROUNDS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_small(const uint2* __restrict__ ranges, uint32_t* __restrict__ pval,
                                                              const uint32_t* __restrict__ pkey,
                                                              const unsigned long long* __restrict__ key,
-                                                             const uint32_t* __restrict__ orig) {
+                                                             const uint32_t* __restrict__ orig,
+                                                             const DevCounters* gate, unsigned long long pair_cap) {
     extern __shared__ uint32_t smem[];
+    if (gate && gate->pairs_total > pair_cap) return;
     const uint2 r = ranges[blockIdx.x];
     const int L = static_cast<int>(r.y - r.x);
     if (L <= 1 || L > THREADS * ROUNDS) return;
@@ -155,7 +157,8 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
     if (max_len <= 1 || n_tiles == 0) return true;
     if (max_len > kMaxBucketSorted) return false;
     using S1 = TileSortSmem<128, 16>;
-    k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig);
+    k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.gate,
+                                                                  f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > kBlendSortCap) {
         using S2 = TileSortSmem<512, 8>;

@@ -77,6 +77,10 @@ struct ps_ctx {
     DevCounters* h_ctr = nullptr; // pinned
     void* stage = nullptr;        // scene upload staging
     size_t stage_bytes = 0;
+    // image metrics / compare: accumulators and the two framebuffers
+    void* metrics_acc = nullptr;
+    void* cmp_block = nullptr;
+    size_t cmp_bytes = 0;
 };
 
 namespace {
@@ -671,7 +675,8 @@ void ps_ctx_destroy(ps_ctx* c) {
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
     void* bufs[] = {c->n_block, c->p_block, c->radix_scratch, c->scan_scratch, c->img_rgb, c->img_t,
-                    c->f.flags, c->f.ranges, c->f.tile_count, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage};
+                    c->f.flags, c->f.ranges, c->f.tile_count, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage,
+                    c->metrics_acc, c->cmp_block};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
@@ -929,6 +934,76 @@ int ps_tile_lists(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_c
         CTX_TRY(c, cudaMemcpy(orig.data(), s->dev.orig, sizeof(uint32_t) * s->n, cudaMemcpyDeviceToHost));
         for (int64_t k = 0; k < r.pairs; ++k) splat_index[k] = orig[splat_index[k]];
     }
+    return PS_OK;
+}
+
+namespace {
+
+// device buffers for two framebuffers (rgb + T) of `bytes_per_elem`-sized values
+int ensure_cmp(ps_ctx* c, int64_t pix, size_t elem) {
+    const size_t need = 2 * 4 * static_cast<size_t>(pix) * elem + 256;
+    if (!c->metrics_acc) CTX_TRY(c, cudaMalloc(&c->metrics_acc, ps::metrics_scratch_bytes()));
+    if (need > c->cmp_bytes) {
+        if (c->cmp_block) cudaFree(c->cmp_block);
+        c->cmp_block = nullptr;
+        c->cmp_bytes = 0;
+        CTX_TRY(c, cudaMalloc(&c->cmp_block, need));
+        c->cmp_bytes = need;
+    }
+    return PS_OK;
+}
+
+} // namespace
+
+int ps_image_metrics_compute(ps_ctx* c, int width, int height, const void* rgb_a, const void* t_a,
+                             const void* rgb_b, const void* t_b, int dtype, int memspace, const double* bg,
+                             ps_image_metrics* out) {
+    if (!c || !out || !rgb_a || !t_a || !rgb_b || !t_b) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    if (width < 0 || height < 0 || (dtype != PS_DTYPE_F32 && dtype != PS_DTYPE_F64))
+        return set_err(c, PS_INVALID_ARGUMENT, "bad image size or dtype");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    const int64_t pix = static_cast<int64_t>(width) * height;
+    const size_t elem = dtype == PS_DTYPE_F64 ? sizeof(double) : sizeof(float);
+    int st = ensure_cmp(c, pix, elem);
+    if (st != PS_OK) return st;
+    const void* p[4] = {rgb_a, t_a, rgb_b, t_b};
+    if (memspace == PS_MEM_HOST) {
+        char* q = static_cast<char*>(c->cmp_block);
+        const size_t sz[4] = {3 * pix * elem, pix * elem, 3 * pix * elem, pix * elem};
+        for (int k = 0; k < 4; ++k) {
+            CTX_TRY(c, cudaMemcpyAsync(q, p[k], sz[k], cudaMemcpyHostToDevice, c->stream));
+            p[k] = q;
+            q += (sz[k] + 255) & ~size_t(255);
+        }
+    }
+    const double white[3] = {1.0, 1.0, 1.0};
+    if (ps::launch_image_metrics(p[0], p[1], p[2], p[3], dtype == PS_DTYPE_F64, width, height, bg ? bg : white,
+                                 c->metrics_acc, out, c->stream) != 0)
+        CTX_TRY(c, cudaGetLastError());
+    CTX_TRY(c, cudaGetLastError());
+    return PS_OK;
+}
+
+int ps_compare(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg_a, const ps_config* cfg_b,
+               const double* bg, ps_compare_report* out) {
+    if (!c || !s || !cam || !cfg_a || !cfg_b || !out) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    const int64_t pix = static_cast<int64_t>(cam->width) * cam->height;
+    int st = ensure_cmp(c, pix, sizeof(float));
+    if (st != PS_OK) return st;
+    float* a_rgb = static_cast<float*>(c->cmp_block);
+    float* a_t = a_rgb + 3 * pix;
+    float* b_rgb = a_t + pix;
+    float* b_t = b_rgb + 3 * pix;
+    if ((st = render_one(c, s, cam, cfg_a, a_rgb, a_t, PS_MEM_DEVICE, &out->counters_a, false, nullptr)) != PS_OK)
+        return st;
+    if ((st = render_one(c, s, cam, cfg_b, b_rgb, b_t, PS_MEM_DEVICE, &out->counters_b, false, nullptr)) != PS_OK)
+        return st;
+    if ((st = ps_image_metrics_compute(c, cam->width, cam->height, a_rgb, a_t, b_rgb, b_t, PS_DTYPE_F32,
+                                       PS_MEM_DEVICE, bg, &out->metrics)) != PS_OK)
+        return st;
+    const uint64_t pa = out->counters_a.tile_pairs_after_tight_test;
+    out->pair_ratio = pa ? static_cast<double>(out->counters_b.tile_pairs_after_tight_test) / static_cast<double>(pa)
+                         : 0.0;
     return PS_OK;
 }
 

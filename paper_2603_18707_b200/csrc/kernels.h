@@ -73,6 +73,12 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
                            cudaStream_t st, int* launches);
 
+// metrics.cu — composite + PSNR / max-abs / SSIM of two framebuffers
+// (fp32 or fp64, device pointers) against background bg; synchronises st.
+size_t metrics_scratch_bytes();
+int launch_image_metrics(const void* rgb_a, const void* t_a, const void* rgb_b, const void* t_b, bool f64, int W,
+                         int H, const double bg[3], void* scratch, ps_image_metrics* out, cudaStream_t st);
+
 // utils.cu
 void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st);
 // scene reordering along a 30-bit Morton curve of the means (upload time)

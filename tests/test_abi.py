@@ -42,8 +42,9 @@ PROBE = r"""
 #include <stddef.h>
 #include "polysplat_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(ps_kernel), sizeof(ps_config), sizeof(ps_camera),
-         sizeof(ps_counters), sizeof(ps_stats), sizeof(ps_prepared));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ps_kernel), sizeof(ps_config), sizeof(ps_camera),
+         sizeof(ps_counters), sizeof(ps_stats), sizeof(ps_prepared), sizeof(ps_image_metrics),
+         sizeof(ps_compare_report));
   printf("%zu %zu %zu %zu\n", offsetof(ps_config, kernel), offsetof(ps_config, culling_kernel),
          offsetof(ps_config, v_dilation), offsetof(ps_camera, rotation));
   return 0;
@@ -58,7 +59,7 @@ def test_pod_layouts_match_ctypes(tmp_path):
     subprocess.run(["gcc", "-std=c99", f"-I{ROOT}/include", str(src), "-o", str(exe)], check=True)
     sizes, offs = subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines()
     want = [C.sizeof(t) for t in (abi.ps_kernel, abi.ps_config, abi.ps_camera, abi.ps_counters, abi.ps_stats,
-                                  abi.ps_prepared)]
+                                  abi.ps_prepared, abi.ps_image_metrics, abi.ps_compare_report)]
     assert [int(x) for x in sizes.split()] == want
     assert [int(x) for x in offs.split()] == [abi.ps_config.kernel.offset, abi.ps_config.culling_kernel.offset,
                                               abi.ps_config.v_dilation.offset, abi.ps_camera.rotation.offset]

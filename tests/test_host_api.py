@@ -151,3 +151,23 @@ def test_default_config_matches_reference_defaults():
     d = abi.default_config()
     assert bytes(c) == bytes(d)
     assert c.tile_size == 16 and abs(c.epsilon - 1 / 255) == 0 and c.transmittance_floor == 1e-4
+
+
+def test_csv_rows_match_reference_format():
+    """metrics.cpp csv_header / csv_row / fmt17 (%.17g, inf spelled out)."""
+    ctr_a = api.PerfCounters(**{k: 0 for k in api.PerfCounters.__dataclass_fields__})
+    ctr_b = api.PerfCounters(**{k: 0 for k in api.PerfCounters.__dataclass_fields__})
+    ctr_a.tile_pairs_after_tight_test, ctr_b.tile_pairs_after_tight_test = 24725, 20000
+    r = api.CompareReport(api.ImageMetrics(math.inf, 0.1, 1.0 / 3.0), ctr_a, ctr_b, 20000 / 24725)
+    assert api.csv_header() == "label_a,label_b,psnr_db,ssim,max_abs_diff,pairs_a,pairs_b,pair_ratio\n"
+    row = api.csv_row("exp/stp", "poly1/opacity", r)
+    assert row == ("exp/stp,poly1/opacity,inf,0.10000000000000001,0.33333333333333331,24725,20000,"
+                   "0.80889787664307378\n")
+    assert float(row.split(",")[4]) == 1.0 / 3.0  # round-trips exactly
+
+
+def test_reference_ssim_of_identical_images(reference):
+    rgb = np.random.default_rng(0).uniform(0, 1, (16, 20, 3))
+    t = np.zeros((16, 20))
+    p, m, s = reference.compare_images(rgb, t, rgb, t, with_ssim=True)
+    assert p == math.inf and m == 0.0 and s == pytest.approx(1.0, abs=1e-12)
