@@ -254,11 +254,21 @@ def run_ours(args) -> None:
 
     # poly-vs-exp and the rest of the kernel matrix (fewer steps each)
     if not args.no_compare:
-        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms / frames_per_step}}
+        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms / frames_per_step, "pairs": st["pairs"]}}
         for label, kname, mode in COMPARE:
             c2 = make_cfg(api, kname, mode, deg).to_struct()
             m2, _, _, _ = timed(c2, max(3, min(args.steps, 10)), 3)
-            kern[label] = {"frames_per_s": frames_per_step * 1000.0 / m2, "ms": m2 / frames_per_step}
+            kern[label] = {"frames_per_s": frames_per_step * 1000.0 / m2, "ms": m2 / frames_per_step,
+                           "pairs": r.stats()["pairs"]}
+        # image quality of every kernel against exp / StopThePop (the paper's
+        # comparison point), on the device: polysplat::compare (metrics.cpp:138-157)
+        ref_cfg = make_cfg(api, "exp", "StopThePop", deg)
+        for label, kname, mode in [HEADLINE] + COMPARE:
+            if label == "exp/stp":
+                continue
+            rep = r.compare(ds, cam, ref_cfg, make_cfg(api, kname, mode, deg))
+            kern[label].update({"psnr_vs_exp_db": rep.psnr_db, "ssim_vs_exp": rep.ssim,
+                                "pair_ratio_vs_exp": rep.pair_ratio})
         result["kernels"] = kern
         result["poly1_vs_exp_speedup"] = kern["exp/stp"]["ms"] / kern[HEADLINE[0]]["ms"]
 

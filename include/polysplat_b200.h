@@ -50,7 +50,10 @@ extern "C" {
  *   PS_EPSILON_ZERO_UNBOUNDED    -> polysplat::EpsilonZeroUnbounded
  *   PS_FULLY_CULLED              -> polysplat::FullyCulled (culling_radius only)
  *   PS_ERROR                     -> polysplat::Error
- *   PS_CUDA_ERROR / PS_OUT_OF_MEMORY -> std::runtime_error (no reference analogue) */
+ *   PS_CUDA_ERROR / PS_OUT_OF_MEMORY -> std::runtime_error (no reference analogue)
+ *   PS_IO_ERROR / PS_MALFORMED_HEADER / PS_UNSUPPORTED_FORMAT / PS_MISSING_PROPERTY /
+ *   PS_TRUNCATED_DATA -> polysplat::IoError / MalformedHeader / UnsupportedFormat /
+ *                        MissingProperty / TruncatedData (load_ply, scene_io.cpp:53-199) */
 typedef enum ps_status {
     PS_OK = 0,
     PS_INVALID_ARGUMENT = 1,
@@ -61,7 +64,12 @@ typedef enum ps_status {
     PS_FULLY_CULLED = 6,
     PS_ERROR = 7,
     PS_CUDA_ERROR = 8,
-    PS_OUT_OF_MEMORY = 9
+    PS_OUT_OF_MEMORY = 9,
+    PS_IO_ERROR = 10,
+    PS_MALFORMED_HEADER = 11,
+    PS_UNSUPPORTED_FORMAT = 12,
+    PS_MISSING_PROPERTY = 13,
+    PS_TRUNCATED_DATA = 14
 } ps_status;
 
 /* kernel.hpp:12-17 KernelKind */
@@ -184,6 +192,21 @@ int ps_scene_update_soa(ps_ctx* ctx, ps_scene* scene, const double* means, const
                         const double* rotations, const double* opacities, const float* sh,
                         int memspace);
 int64_t ps_scene_size(const ps_scene* scene);
+
+/* 3DGS checkpoints (load_ply, scene_io.cpp:53-199; scene_io.hpp:23-27): binary
+ * little-endian PLY with float32 x,y,z,f_dc_0..2,f_rest_*,opacity,scale_0..2,
+ * rot_0..3 (other properties skipped by stride). The activations
+ * (sigmoid(opacity), exp(scale), normalized quaternion) run on the host in
+ * fp64 with the reference's expressions, so the fields equal the reference's
+ * Splat3D bit for bit. SH degree from the f_rest count (9/24/45 -> 1/2/3).
+ * ps_ply_info: header only. ps_ply_load_soa / _splat3d: host arrays of
+ * `capacity` splats (SoA as ps_scene_create_soa, or Splat3D records).
+ * ps_scene_load_ply: straight into a device scene. */
+int ps_ply_info(const char* path, int64_t* n_out, int* sh_degree);
+int ps_ply_load_soa(const char* path, double* means, double* scales, double* rotations, double* opacities,
+                    float* sh, int64_t capacity, int64_t* n_out, int* sh_degree);
+int ps_ply_load_splat3d(const char* path, double* splats, int64_t capacity, int64_t* n_out, int* sh_degree);
+int ps_scene_load_ply(ps_ctx* ctx, const char* path, ps_scene** out, int* sh_degree);
 void ps_scene_destroy(ps_scene* scene);
 
 /* ---------------------------------------------------------------- render

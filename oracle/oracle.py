@@ -222,6 +222,11 @@ class Reference(_Lib):
         L.ref_compare_images.argtypes = [C.c_int, C.c_int] + [C.POINTER(C.c_double)] * 5 + [
             C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_compare_images.restype = C.c_int
+        L.ref_load_ply.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int)]
+        L.ref_load_ply.restype = C.c_int
+        L.ref_write_ply.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int, C.c_char_p]
+        L.ref_write_ply.restype = C.c_int
         L.ref_resolve_thread_count.argtypes = [C.c_int]
         L.ref_resolve_thread_count.restype = C.c_int
 
@@ -258,6 +263,18 @@ class Reference(_Lib):
         self._call("compare_images", w, h, *[dptr(a) for a in arrs], C.byref(p), C.byref(m),
                    C.byref(s) if with_ssim else None)
         return (p.value, m.value, s.value) if with_ssim else (p.value, m.value)
+
+    def load_ply(self, path):
+        """load_ply -> (Splat3D array (n, 59), sh_degree); raises OracleError(status, msg)."""
+        n, deg = C.c_int64(0), C.c_int(0)
+        self._call("load_ply", str(path).encode(), None, 0, C.byref(n), C.byref(deg))
+        out = np.zeros((n.value, abi.SPLAT3D_DOUBLES))
+        self._call("load_ply", str(path).encode(), dptr(out), n.value, C.byref(n), C.byref(deg))
+        return out, deg.value
+
+    def write_ply(self, splats, sh_degree, path):
+        a = np.ascontiguousarray(splats, dtype=np.float64)
+        self._call("write_ply", dptr(a), len(a), sh_degree, str(path).encode())
 
     def resolve_thread_count(self, requested: int = 0) -> int:
         return self.lib.ref_resolve_thread_count(requested)

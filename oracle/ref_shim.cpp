@@ -46,6 +46,16 @@ int guarded(F&& f) {
         return fail(PS_EPSILON_ZERO_UNBOUNDED, e.what());
     } catch (const FullyCulled& e) {
         return fail(PS_FULLY_CULLED, e.what());
+    } catch (const IoError& e) {
+        return fail(PS_IO_ERROR, e.what());
+    } catch (const MalformedHeader& e) {
+        return fail(PS_MALFORMED_HEADER, e.what());
+    } catch (const UnsupportedFormat& e) {
+        return fail(PS_UNSUPPORTED_FORMAT, e.what());
+    } catch (const MissingProperty& e) {
+        return fail(PS_MISSING_PROPERTY, e.what());
+    } catch (const TruncatedData& e) {
+        return fail(PS_TRUNCATED_DATA, e.what());
     } catch (const Error& e) {
         return fail(PS_ERROR, e.what());
     } catch (const std::invalid_argument& e) {
@@ -359,6 +369,31 @@ int ref_tile_rect(double mx, double my, const double cov_aa[3], double radius_si
 double ref_min_quadric_over_box(const double conic[3], double mx, double my, const double box[4]) {
     return min_quadric_over_box(Sym2{conic[0], conic[1], conic[2]}, Vec2{mx, my},
                                 PixelBox{box[0], box[1], box[2], box[3]});
+}
+
+// load_ply (scene_io.cpp:53-199): Splat3D records; with splats == NULL only n / degree
+int ref_load_ply(const char* path, double* splats, int64_t capacity, int64_t* n_out, int* sh_degree) {
+    return guarded([&]() -> int {
+        SceneFile sf = load_ply(path);
+        *n_out = static_cast<int64_t>(sf.splats.size());
+        *sh_degree = sf.sh_degree;
+        if (splats) {
+            if (*n_out > capacity) return fail(PS_INVALID_ARGUMENT, "capacity too small");
+            std::memcpy(splats, sf.splats.data(), sizeof(Splat3D) * sf.splats.size());
+        }
+        return PS_OK;
+    });
+}
+
+// write_ply (scene_io.cpp:201-238)
+int ref_write_ply(const double* splats, int64_t n, int sh_degree, const char* path) {
+    return guarded([&]() -> int {
+        SceneFile sf;
+        sf.splats.assign(reinterpret_cast<const Splat3D*>(splats), reinterpret_cast<const Splat3D*>(splats) + n);
+        sf.sh_degree = sh_degree;
+        write_ply(sf, path);
+        return PS_OK;
+    });
 }
 
 // composite + psnr / max_abs_diff / ssim (metrics.cpp:13-134), background (bg[3]); ssim_out may be NULL

@@ -25,6 +25,7 @@ EXPORTS = (
     "ps_first_positive_root", "ps_culling_radius", "ps_eval_kernel", "ps_validate_config",
     "ps_validate_camera", "ps_default_config", "ps_synth_scene", "ps_synth_scene_soa",
     "ps_orbit_cameras", "ps_image_metrics_compute", "ps_compare",
+    "ps_ply_info", "ps_ply_load_soa", "ps_ply_load_splat3d", "ps_scene_load_ply",
 )
 
 _lib = None
@@ -61,6 +62,10 @@ def _declare(L) -> None:
         "ps_image_metrics_compute": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, dp,
                                               P(abi.ps_image_metrics)]),
         "ps_compare": (C.c_int, [vp, vp, cam_p, cfg_p, cfg_p, dp, P(abi.ps_compare_report)]),
+        "ps_ply_info": (C.c_int, [C.c_char_p, P(i64), P(C.c_int)]),
+        "ps_ply_load_soa": (C.c_int, [C.c_char_p, dp, dp, dp, dp, fp, i64, P(i64), P(C.c_int)]),
+        "ps_ply_load_splat3d": (C.c_int, [C.c_char_p, dp, i64, P(i64), P(C.c_int)]),
+        "ps_scene_load_ply": (C.c_int, [vp, C.c_char_p, P(vp), P(C.c_int)]),
         "ps_make_polynomial_kernel": (C.c_int, [C.c_int, dp, C.c_int, P(abi.ps_kernel)]),
         "ps_make_exponential_kernel": (abi.ps_kernel, []),
         "ps_first_positive_root": (C.c_int, [dp, C.c_int, dp]),

@@ -26,6 +26,7 @@ PS_FULLY_CULLED = 6
 PS_ERROR = 7
 PS_CUDA_ERROR = 8
 PS_OUT_OF_MEMORY = 9
+PS_IO_ERROR, PS_MALFORMED_HEADER, PS_UNSUPPORTED_FORMAT, PS_MISSING_PROPERTY, PS_TRUNCATED_DATA = 10, 11, 12, 13, 14
 
 # KernelKind (kernel.hpp:12-17)
 PS_KERNEL_EXPONENTIAL = 0

@@ -52,6 +52,26 @@ class NonOrthonormalRotation(Error):
     pass
 
 
+class IoError(Error):
+    pass
+
+
+class MalformedHeader(Error):
+    pass
+
+
+class UnsupportedFormat(Error):
+    pass
+
+
+class MissingProperty(Error):
+    pass
+
+
+class TruncatedData(Error):
+    pass
+
+
 class InvalidArgument(ValueError):
     """std::invalid_argument"""
 
@@ -70,6 +90,11 @@ _STATUS = {
     abi.PS_ERROR: Error,
     abi.PS_CUDA_ERROR: DeviceError,
     abi.PS_OUT_OF_MEMORY: DeviceError,
+    abi.PS_IO_ERROR: IoError,
+    abi.PS_MALFORMED_HEADER: MalformedHeader,
+    abi.PS_UNSUPPORTED_FORMAT: UnsupportedFormat,
+    abi.PS_MISSING_PROPERTY: MissingProperty,
+    abi.PS_TRUNCATED_DATA: TruncatedData,
 }
 
 
@@ -319,6 +344,31 @@ class Scene:
         return Scene(means, scales, rots, opac, sh, deg.value)
 
 
+def load_ply(path: str) -> Scene:
+    """load_ply (scene_io.cpp:53-199): a 3DGS checkpoint as a Scene (SoA), with
+    the reference's activations applied in fp64 (bit-identical fields)."""
+    n, deg = C.c_int64(0), C.c_int(0)
+    p = str(path).encode()
+    _check(lib().ps_ply_info(p, C.byref(n), C.byref(deg)))
+    m = n.value
+    means, scales = np.zeros((m, 3)), np.zeros((m, 3))
+    rots, opac = np.zeros((m, 4)), np.zeros(m)
+    sh = np.zeros((m, 16, 3), np.float32)
+    _check(lib().ps_ply_load_soa(p, abi.dptr(means), abi.dptr(scales), abi.dptr(rots), abi.dptr(opac),
+                                 sh.ctypes.data_as(C.POINTER(C.c_float)), m, C.byref(n), C.byref(deg)))
+    return Scene(means, scales, rots, opac, sh, deg.value)
+
+
+def load_ply_splat3d(path: str):
+    """load_ply as the reference's SceneFile: (Splat3D array (n, 59) f64, sh_degree)."""
+    n, deg = C.c_int64(0), C.c_int(0)
+    p = str(path).encode()
+    _check(lib().ps_ply_info(p, C.byref(n), C.byref(deg)))
+    out = np.zeros((n.value, abi.SPLAT3D_DOUBLES))
+    _check(lib().ps_ply_load_splat3d(p, abi.dptr(out), n.value, C.byref(n), C.byref(deg)))
+    return out, deg.value
+
+
 def synthetic_splat3d(kind: int, seed: int = 0, n: int = 0):
     """The scene as a reference Splat3D array (n, 59) f64 plus its SH degree."""
     cnt = C.c_int64(0)
@@ -409,6 +459,14 @@ class Rasterizer:
         _check(lib().ps_scene_create_soa(self.handle, *[a.ctypes.data for a in arrs], n, abi.PS_MEM_HOST,
                                          C.byref(h)), self.handle)
         return DeviceScene(self, h, n)
+
+    def upload_ply(self, path: str) -> DeviceScene:
+        """ps_scene_load_ply: a 3DGS checkpoint straight into a device scene."""
+        h, deg = C.c_void_p(), C.c_int(0)
+        _check(lib().ps_scene_load_ply(self.handle, str(path).encode(), C.byref(h), C.byref(deg)), self.handle)
+        ds = DeviceScene(self, h, lib().ps_scene_size(h))
+        ds.sh_degree = deg.value
+        return ds
 
     def upload_splat3d(self, splats: np.ndarray) -> DeviceScene:
         a = np.ascontiguousarray(splats, dtype=np.float64)

@@ -48,6 +48,7 @@ SOURCES = [
     ("context.cu", []),
     ("hostmath.cpp", []),
     ("synth.cpp", []),
+    ("ply.cpp", []),
 ]
 HEADERS = ["common.cuh", "exact_math.cuh", "kernels.h", "tile_sort.cuh"]
 
@@ -66,7 +67,7 @@ def _stale(obj: str, src: str) -> bool:
     if not os.path.exists(obj):
         return True
     t = os.path.getmtime(obj)
-    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [
+    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(CSRC, "exports.map"),
         os.path.join(INCLUDE, "polysplat_b200.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -95,7 +96,8 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
                 if verbose:
                     print(f"  compiled {src}", file=sys.stderr)
     if todo or not os.path.exists(LIB):
-        link = [_nvcc(), "-ccbin", _host_cxx(), "-shared", *ARCH, "-o", LIB, *objs, "-cudart", "static"]
+        link = [_nvcc(), "-ccbin", _host_cxx(), "-shared", *ARCH, "-o", LIB, *objs, "-cudart", "static",
+                "-Xlinker", f"--version-script={os.path.join(CSRC, 'exports.map')}"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -1007,4 +1007,19 @@ int ps_compare(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_conf
     return PS_OK;
 }
 
+int ps_scene_load_ply(ps_ctx* c, const char* path, ps_scene** out, int* sh_degree) {
+    if (!c || !out) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    int64_t n = 0;
+    int deg = 0;
+    int st = ps_ply_info(path, &n, &deg);
+    if (st != PS_OK) return set_err(c, st, g_free_error);
+    std::vector<double> means(3 * n), scales(3 * n), rots(4 * n), opac(n);
+    std::vector<float> sh(48 * n);
+    st = ps_ply_load_soa(path, means.data(), scales.data(), rots.data(), opac.data(), sh.data(), n, &n, &deg);
+    if (st != PS_OK) return set_err(c, st, g_free_error);
+    if (sh_degree) *sh_degree = deg;
+    return ps_scene_create_soa(c, means.data(), scales.data(), rots.data(), opac.data(), sh.data(), n, PS_MEM_HOST,
+                               out);
+}
+
 } // extern "C"
