@@ -190,8 +190,21 @@ def run_ours(args) -> None:
     cam_s = cam.to_struct()
 
     cam_structs = [cams[v].to_struct() for v in my_views]
+    # several views per step: one ps_render_views call (K1 fused over batches of
+    # views, each view's binning / blend on its own stream) into per-view outputs
+    batch = len(cam_structs) > 1
+    if batch:
+        cam_arr = (type(cam_structs[0]) * len(cam_structs))(*cam_structs)
+        out_rgb = torch.empty((len(cam_structs), h, w, 3), dtype=torch.float32, device="cuda")
+        out_t = torch.empty((len(cam_structs), h, w), dtype=torch.float32, device="cuda")
 
     def render_dev(cfg_s):
+        if batch:
+            st = lib.ps_render_views(r.handle, ds.handle, cam_arr, len(cam_structs), C.byref(cfg_s),
+                                     out_rgb.data_ptr(), out_t.data_ptr(), 1, None)
+            if st != 0:
+                raise RuntimeError(api.last_error(r.handle))
+            return
         for cs in cam_structs:
             st = lib.ps_render(r.handle, ds.handle, C.byref(cs), C.byref(cfg_s), out_rgb.data_ptr(),
                                out_t.data_ptr(), 1, None)
@@ -227,7 +240,8 @@ def run_ours(args) -> None:
         r.set_timing(False)
         ms = sum(a.elapsed_time(b) for a, b in evs) / steps
         ms = max_over_ranks(ms, dist, device="cuda")
-        stages = {k: v / steps for k, v in stage_sum.items()}
+        # per frame (a batched step reports its views' summed stage times)
+        stages = {k: v / steps / frames_per_step for k, v in stage_sum.items()}
         return ms, stages, launches, (sampler.summary() if sampler else None)
 
     cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg)
@@ -250,7 +264,8 @@ def run_ours(args) -> None:
                       "exact_alpha_evals": st["exact_alpha_evals"]}
 
     if rank == 0:
-        result["roofline"], result["roofline_stages"] = roofline(r, stages, n, deg, st, ctr, HEADLINE[1])
+        result["roofline"], result["roofline_stages"] = roofline(r, stages, n, deg, st, ctr, HEADLINE[1],
+                                                                 args.workload)
 
     # poly-vs-exp and the rest of the kernel matrix (fewer steps each)
     if not args.no_compare:
@@ -359,7 +374,7 @@ def run_ours(args) -> None:
         print(json.dumps(result), flush=True)
 
 
-def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
+def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workload: str = "c2"):
     """Per-stage achieved vs peak; the dominant stage goes to the top-level `roofline`."""
     import ctypes as C
 
@@ -398,7 +413,7 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
     top = dict(out[dom]) if dom else {}
     if dom:
         top["kernel"] = dom
-        top["traffic"], top["traffic_source"] = profiled_traffic(dom, kname)
+        top["traffic"], top["traffic_source"] = profiled_traffic(dom, kname, workload)
         top["peak_note"] = ("HBM peak from MEASURED_PEAKS.json" if top["bound"] == "hbm"
                             else "FP32 issue peak measured in-run (no FP32 entry in MEASURED_PEAKS.json)")
     return top, out
@@ -408,15 +423,15 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str):
 _STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0", "preprocess": "k_geometry", "duplicate": "k_duplicate_buckets"}
 
 
-def profiled_traffic(stage: str, kname: str):
+def profiled_traffic(stage: str, kname: str, workload: str = "c2"):
     """DRAM bytes (read + write) per launch of the stage's kernel, from the
     newest committed `ncu --set full` capture of C2 (profiles/*_ncu_full_c2_raw.csv),
     or (None, reason)."""
     import csv
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full_c2_raw.csv")))
-    if not files or kname != "poly1" or stage not in _STAGE_KERNEL:
-        return None, "no matching ncu capture"
+    if not files or kname != "poly1" or stage not in _STAGE_KERNEL or workload != "c2":
+        return None, "no matching ncu capture (C2 only)"
     rows = list(csv.reader(open(files[-1])))
     hdr, units = rows[0], rows[1]
     try:

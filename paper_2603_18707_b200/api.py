@@ -498,6 +498,27 @@ class Rasterizer:
             if tmp:
                 ds.close()
 
+    def render_views(self, scene, cams: Sequence[Camera], cfg: RasterConfig, counters: bool = True):
+        """ps_render_views: a batch of views of one scene (K1 fused over up to 4
+        views at a time). Returns a list of (Framebuffer, PerfCounters)."""
+        ds, tmp = self._scene(scene)
+        try:
+            n = len(cams)
+            if n == 0:
+                return []
+            w, h = cams[0].width, cams[0].height
+            cs = (abi.ps_camera * n)(*[c.to_struct() for c in cams])
+            g = cfg.to_struct()
+            rgb = np.zeros((n, h, w, 3), np.float32)
+            tr = np.zeros((n, h, w), np.float32)
+            ctr = (abi.ps_counters * n)()
+            _check(lib().ps_render_views(self.handle, ds.handle, cs, n, C.byref(g), rgb.ctypes.data, tr.ctypes.data,
+                                         abi.PS_MEM_HOST, ctr if counters else None), self.handle)
+            return [(Framebuffer(w, h, rgb[k], tr[k]), PerfCounters.from_struct(ctr[k])) for k in range(n)]
+        finally:
+            if tmp:
+                ds.close()
+
     def render_splat3d(self, splats: np.ndarray, cam: Camera, cfg: RasterConfig):
         """One-shot drop-in (ps_render_splats): fp64 framebuffer with exact replayed pixels."""
         a = np.ascontiguousarray(splats, dtype=np.float64)

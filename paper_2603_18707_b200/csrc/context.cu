@@ -81,6 +81,10 @@ struct ps_ctx {
     void* metrics_acc = nullptr;
     void* cmp_block = nullptr;
     size_t cmp_bytes = 0;
+    // view batches (ps_render_views): one child context per fused view, each
+    // with its own frame arrays, counters and stream
+    std::vector<ps_ctx*> views;
+    cudaEvent_t k1_event = nullptr;
 };
 
 namespace {
@@ -243,9 +247,15 @@ struct FrameRequest {
     bool count_work = false;
     bool want_replay_vals = false;
     bool no_speculation = false; // force the synchronous (sized) path
+    bool k1_done = false;        // K1 (and the counter / tile-count zeroing) already issued by a view batch
+    bool defer = false;          // speculative path: return kPending instead of the end-of-frame sync
 };
 
+// run_frame status: the speculative frame is queued, finish_frame() completes it
+constexpr int kPending = 1000;
+
 struct FrameResult {
+    int launches = 0;            // kernels launched so far (deferred frames)
     int64_t visible = 0;
     int64_t pairs = 0;
     bool pairs_in_alt = false;
@@ -257,8 +267,8 @@ void record(ps_ctx* c, int stage) {
     if (c->timing) cudaEventRecord(c->ev[stage], c->stream);
 }
 
-int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_config& cfg_in,
-              const FrameRequest& req, FrameResult& res) {
+// Validation and the per-frame parameter block (camera, config, kernel classes).
+int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode mode, FrameParams& P) {
     int st = host_validate_config(cfg_in);
     if (st != PS_OK) return set_err(c, st, "RasterConfig::validate: invalid configuration");
     st = host_validate_camera(cam);
@@ -268,7 +278,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     ps_config cfg = cfg_in;
     if (cfg.sh_degree > 3) cfg.sh_degree = 3;
     if (cfg.sh_degree < 0) cfg.sh_degree = -1;
-    if ((req.mode == Mode::Render) && cfg.tile_size > 32)
+    if ((mode == Mode::Render) && cfg.tile_size > 32)
         return set_err(c, PS_INVALID_ARGUMENT, "device blend supports tile_size <= 32");
     if (cfg.kernel.kind != PS_KERNEL_EXPONENTIAL && (cfg.kernel.order < 1 || cfg.kernel.order > 3))
         return set_err(c, PS_INVALID_ARGUMENT, "kernel order must be in {1,2,3}");
@@ -276,8 +286,6 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         (cfg.culling_kernel.order < 1 || cfg.culling_kernel.order > 3))
         return set_err(c, PS_INVALID_ARGUMENT, "culling kernel order must be in {1,2,3}");
 
-    const int64_t n = s->n;
-    FrameParams P;
     std::memset(&P, 0, sizeof P);
     P.cam = cam;
     P.cfg = cfg;
@@ -308,6 +316,76 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
             P.blend_class = nt == 2 ? 1 : nt == 3 ? 2 : nt == 4 ? 3 : 4;
         }
     }
+    return PS_OK;
+}
+
+int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_config& cfg_in,
+              const FrameRequest& req, FrameResult& res);
+
+// Counter checks after a frame's end-of-frame (or mid-frame) readback: device
+// errors, and the count scan's pair total against the tight-pair count.
+int check_frame_counters(ps_ctx* c, const ps_scene* s, FrameResult& res) {
+    res.ctr = *c->h_ctr;
+    res.visible = static_cast<int64_t>(res.ctr.visible);
+    res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
+    if (res.ctr.error) {
+        uint32_t orig_index = res.ctr.error_index;
+        cudaMemcpy(&orig_index, s->dev.orig + res.ctr.error_index, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
+                      orig_index);
+        return set_err(c, static_cast<int>(res.ctr.error), buf);
+    }
+    if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
+        return set_err(c, PS_ERROR, "internal: pair scan disagrees with tight count");
+    return PS_OK;
+}
+
+void frame_stats(ps_ctx* c, const FrameResult& res) {
+    c->stats.visible = res.visible;
+    c->stats.pairs = res.pairs;
+    c->stats.replay_pixels = res.ctr.replay_px;
+    c->stats.exact_alpha_evals = res.ctr.exact_evals;
+    c->stats.kernel_launches = res.launches;
+    if (c->timing) {
+        for (int k = 0; k < PS_STAGE_COUNT; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
+            c->stats.stage_ms[k] = ms;
+        }
+    }
+}
+
+// Completes a speculative frame: one sync, the counter checks, and a sized
+// re-run when the frame outgrew the pair buffers or met an unannounced long
+// bucket (K1 is re-issued: K2 / K3 consumed its tile counts).
+int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_config& cfg_in,
+                 const FrameRequest& req, FrameResult& res) {
+    CTX_TRY(c, cudaStreamSynchronize(c->stream));
+    CTX_TRY(c, cudaGetLastError());
+    int st = check_frame_counters(c, s, res);
+    if (st != PS_OK) return st;
+    const bool long_sorts = c->last_max_len > kBlendSortCap;
+    c->last_max_len = res.ctr.max_tile_len;
+    if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
+        (!long_sorts && res.ctr.max_tile_len > kBlendSortCap)) {
+        FrameRequest sized = req;
+        sized.no_speculation = true;
+        sized.k1_done = false;
+        sized.defer = false;
+        return run_frame(c, s, cam, cfg_in, sized, res);
+    }
+    frame_stats(c, res);
+    return PS_OK;
+}
+
+int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_config& cfg_in,
+              const FrameRequest& req, FrameResult& res) {
+    FrameParams P;
+    int st = make_params(c, cam, cfg_in, req.mode, P);
+    if (st != PS_OK) return st;
+    const ps_config& cfg = P.cfg;
+    const int64_t n = s->n;
     const int n_tiles = P.tiles_x * P.tiles_y;
     const int64_t pix = static_cast<int64_t>(cam.width) * cam.height;
 
@@ -331,15 +409,15 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
 
     int launches = 0;
     cudaStream_t strm = c->stream;
-    CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
-    if (req.mode != Mode::Prepare)
-        CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * n_tiles, strm));
-    else
-        f.tile_count = nullptr;
+    if (req.mode == Mode::Prepare) f.tile_count = nullptr;
     record(c, 0);
-    // K1: preprocess (+ tight pair count per tile)
-    launch_preprocess(s->dev, P, f, c->d_ctr, strm);
-    launches += n > 0 ? 2 : 0;
+    if (!req.k1_done) {
+        CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
+        if (f.tile_count) CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * n_tiles, strm));
+        // K1: preprocess (+ tight pair count per tile)
+        launch_preprocess(s->dev, P, f, c->d_ctr, strm);
+        launches += n > 0 ? 2 : 0;
+    }
     record(c, 1);
     const uint32_t* order = nullptr;
     if (req.mode == Mode::Prepare) {
@@ -357,36 +435,6 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         launches += 1;
     }
     record(c, 2);
-    auto check_counters = [&]() -> int {
-        res.ctr = *c->h_ctr;
-        res.visible = static_cast<int64_t>(res.ctr.visible);
-        res.pairs = static_cast<int64_t>(res.ctr.pairs_total);
-        if (res.ctr.error) {
-            uint32_t orig_index = res.ctr.error_index;
-            cudaMemcpy(&orig_index, s->dev.orig + res.ctr.error_index, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-            char buf[256];
-            std::snprintf(buf, sizeof buf, "%s (splat %u)", status_message(static_cast<int>(res.ctr.error)),
-                          orig_index);
-            return set_err(c, static_cast<int>(res.ctr.error), buf);
-        }
-        if (static_cast<unsigned long long>(res.pairs) != res.ctr.tight)
-            return set_err(c, PS_ERROR, "internal: pair scan disagrees with tight count");
-        return PS_OK;
-    };
-    auto finish_stats = [&]() {
-        c->stats.visible = res.visible;
-        c->stats.pairs = res.pairs;
-        c->stats.replay_pixels = res.ctr.replay_px;
-        c->stats.exact_alpha_evals = res.ctr.exact_evals;
-        c->stats.kernel_launches = launches;
-        if (c->timing) {
-            for (int k = 0; k < PS_STAGE_COUNT; ++k) {
-                float ms = 0.f;
-                cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
-                c->stats.stage_ms[k] = ms;
-            }
-        }
-    };
     if (req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 && !req.no_speculation &&
         c->last_max_len <= kMaxBucketSorted) {
         // Speculative frame: no host round trip between the count scan and the
@@ -414,24 +462,15 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         record(c, 6);
         record(c, 7);
         CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
-        CTX_TRY(c, cudaStreamSynchronize(strm));
-        CTX_TRY(c, cudaGetLastError());
-        if ((st = check_counters()) != PS_OK) return st;
-        c->last_max_len = res.ctr.max_tile_len;
-        if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
-            (!long_sorts && res.ctr.max_tile_len > kBlendSortCap)) {
-            FrameRequest sized = req;
-            sized.no_speculation = true;
-            return run_frame(c, s, cam, cfg_in, sized, res);
-        }
-        finish_stats();
-        return PS_OK;
+        res.launches = launches;
+        if (req.defer) return kPending; // finish_frame() syncs and checks
+        return finish_frame(c, s, cam, cfg_in, req, res);
     }
     CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
     CTX_TRY(c, cudaStreamSynchronize(strm));
     CTX_TRY(c, cudaGetLastError());
     record(c, 3);
-    if ((st = check_counters()) != PS_OK) return st;
+    if ((st = check_frame_counters(c, s, res)) != PS_OK) return st;
     if (req.mode == Mode::CountPairs || req.mode == Mode::Prepare) {
         c->stats.visible = res.visible;
         c->stats.pairs = res.pairs;
@@ -504,7 +543,8 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     CTX_TRY(c, cudaGetLastError());
     res.ctr = *c->h_ctr;
     c->last_max_len = res.ctr.max_tile_len;
-    finish_stats();
+    res.launches = launches;
+    frame_stats(c, res);
     return PS_OK;
 }
 
@@ -670,7 +710,10 @@ int ps_ctx_create(int device, ps_ctx** out) {
 
 void ps_ctx_destroy(ps_ctx* c) {
     if (!c) return;
+    for (ps_ctx* v : c->views) ps_ctx_destroy(v);
+    c->views.clear();
     cudaSetDevice(c->device);
+    if (c->k1_event) cudaEventDestroy(c->k1_event);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
@@ -782,20 +825,153 @@ int ps_render(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_confi
     return render_one(c, s, cam, cfg, out_rgb, out_t, memspace, counters, false, nullptr);
 }
 
+namespace {
+
+// One in-flight batch of ps_render_views: up to kMaxFusedViews views on one set
+// of child contexts.
+struct ViewBatch {
+    int first = 0, nv = 0;
+    FrameRequest req[ps::kMaxFusedViews];
+    FrameResult res[ps::kMaxFusedViews];
+    int status[ps::kMaxFusedViews];
+};
+
+// Issues batch vb on child-context set `set`: K1 fused over its views on the
+// parent stream, then each view's K2..K6 queued on its child stream (deferred).
+int issue_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, const ps_config* cfg, float* out_rgb,
+                float* out_t, bool dev_out, bool count, int set, ViewBatch& vb, float* k1_ms) {
+    const int G = ps::kMaxFusedViews;
+    const int64_t pix = static_cast<int64_t>(cams[0].width) * cams[0].height;
+    FrameParams P[ps::kMaxFusedViews];
+    FrameDev f[ps::kMaxFusedViews];
+    DevCounters* ctr[ps::kMaxFusedViews];
+    for (int k = 0; k < vb.nv; ++k) {
+        ps_ctx* v = c->views[set * G + k];
+        v->timing = c->timing;
+        int st = make_params(v, cams[vb.first + k], *cfg, Mode::Render, P[k]);
+        if (st != PS_OK) return set_err(c, st, v->err);
+        const int n_tiles = P[k].tiles_x * P[k].tiles_y;
+        if ((st = ensure_frame(v, s->n)) != PS_OK || (st = ensure_image(v, pix, n_tiles)) != PS_OK)
+            return set_err(c, st, v->err);
+        f[k] = v->f;
+        f[k].cov_aa = nullptr;
+        f[k].replay_vals = nullptr;
+        ctr[k] = v->d_ctr;
+        CTX_TRY(c, cudaMemsetAsync(v->d_ctr, 0, sizeof(DevCounters), c->stream));
+        CTX_TRY(c, cudaMemsetAsync(v->f.tile_count, 0, sizeof(uint32_t) * n_tiles, c->stream));
+    }
+    if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+    launch_preprocess_views(s->dev, P, f, ctr, vb.nv, c->stream);
+    if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+    CTX_TRY(c, cudaEventRecord(c->k1_event, c->stream));
+    for (int k = 0; k < vb.nv; ++k) {
+        ps_ctx* v = c->views[set * G + k];
+        CTX_TRY(c, cudaStreamWaitEvent(v->stream, c->k1_event, 0));
+        FrameRequest& rq = vb.req[k];
+        rq = FrameRequest{};
+        rq.mode = Mode::Render;
+        rq.d_rgb = dev_out && out_rgb ? out_rgb + 3 * pix * (vb.first + k) : v->img_rgb;
+        rq.d_t = dev_out && out_t ? out_t + pix * (vb.first + k) : v->img_t;
+        rq.count_work = count;
+        rq.k1_done = true;
+        rq.defer = true;
+        vb.res[k] = FrameResult{};
+        vb.status[k] = run_frame(v, s, cams[vb.first + k], *cfg, rq, vb.res[k]);
+        if (vb.status[k] != PS_OK && vb.status[k] != kPending) return set_err(c, vb.status[k], v->err);
+    }
+    if (c->timing) {
+        float ms = 0.f;
+        cudaEventSynchronize(c->ev[1]);
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        *k1_ms += ms;
+    }
+    return PS_OK;
+}
+
+// Completes batch vb: per-view end-of-frame checks, outputs, counters, stats.
+int finish_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, const ps_config* cfg, float* out_rgb,
+                 float* out_t, bool dev_out, ps_counters* counters, int set, ViewBatch& vb, ps_stats& total) {
+    const int G = ps::kMaxFusedViews;
+    const int64_t pix = static_cast<int64_t>(cams[0].width) * cams[0].height;
+    for (int k = 0; k < vb.nv; ++k) {
+        ps_ctx* v = c->views[set * G + k];
+        if (vb.status[k] == kPending) {
+            const int st = finish_frame(v, s, cams[vb.first + k], *cfg, vb.req[k], vb.res[k]);
+            if (st != PS_OK) return set_err(c, st, v->err);
+        }
+        if (!dev_out) {
+            if (out_rgb)
+                CTX_TRY(c, cudaMemcpyAsync(out_rgb + 3 * pix * (vb.first + k), vb.req[k].d_rgb,
+                                           sizeof(float) * 3 * pix, cudaMemcpyDeviceToHost, v->stream));
+            if (out_t)
+                CTX_TRY(c, cudaMemcpyAsync(out_t + pix * (vb.first + k), vb.req[k].d_t, sizeof(float) * pix,
+                                           cudaMemcpyDeviceToHost, v->stream));
+            CTX_TRY(c, cudaStreamSynchronize(v->stream));
+        }
+        fill_counters(counters ? counters + vb.first + k : nullptr, s, vb.res[k], true);
+        total.visible += v->stats.visible;
+        total.pairs += v->stats.pairs;
+        total.replay_pixels += v->stats.replay_pixels;
+        total.exact_alpha_evals += v->stats.exact_alpha_evals;
+        total.kernel_launches += v->stats.kernel_launches;
+        for (int q = 1; q < PS_STAGE_COUNT; ++q) total.stage_ms[q] += v->stats.stage_ms[q];
+    }
+    total.kernel_launches += 2; // the fused K1a + K1b
+    return PS_OK;
+}
+
+} // namespace
+
 int ps_render_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, int n_views, const ps_config* cfg,
                     float* out_rgb, float* out_t, int memspace, ps_counters* counters) {
-    if (!c || !s || !cams || n_views < 0) return set_err(c, PS_INVALID_ARGUMENT, "bad arguments");
+    if (!c || !s || !cams || !cfg || n_views < 0) return set_err(c, PS_INVALID_ARGUMENT, "bad arguments");
+    if (s->ctx != c) return set_err(c, PS_INVALID_ARGUMENT, "scene belongs to another context");
     for (int v = 0; v < n_views; ++v) {
         if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
             return set_err(c, PS_INVALID_ARGUMENT, "all views must share width/height");
     }
-    const int64_t pix = n_views ? static_cast<int64_t>(cams[0].width) * cams[0].height : 0;
-    for (int v = 0; v < n_views; ++v) {
-        int st = render_one(c, s, &cams[v], cfg, out_rgb ? out_rgb + 3 * pix * v : nullptr,
-                            out_t ? out_t + pix * v : nullptr, memspace, counters ? counters + v : nullptr,
-                            false, nullptr);
-        if (st != PS_OK) return st;
+    if (n_views == 0) return PS_OK;
+    const bool dev_out = memspace == PS_MEM_DEVICE;
+    CTX_TRY(c, cudaSetDevice(c->device));
+    // Views go in batches of up to kMaxFusedViews: K1 is issued once per batch
+    // (each splat's inputs read once for all of its views) on
+    // this context's stream; each view then runs K2..K6 on its own child
+    // context's stream. Two sets of child contexts alternate, so batch b+1's
+    // K1 overlaps batch b's binning / blend.
+    const int G = ps::kMaxFusedViews;
+    const int nb = (n_views + G - 1) / G;
+    const int sets = nb > 1 ? 2 : 1;
+    const int need = (sets - 1) * G + std::min(G, n_views);
+    while (static_cast<int>(c->views.size()) < need) {
+        ps_ctx* v = nullptr;
+        int st = ps_ctx_create(c->device, &v);
+        if (st != PS_OK) return set_err(c, st, "cannot create a view context");
+        c->views.push_back(v);
     }
+    if (!c->k1_event) CTX_TRY(c, cudaEventCreateWithFlags(&c->k1_event, cudaEventDisableTiming));
+    ps_stats total{};
+    float k1_ms = 0.f;
+    ViewBatch vb[2];
+    int st = PS_OK;
+    for (int b = 0; b <= nb && st == PS_OK; ++b) {
+        if (b < nb) {
+            ViewBatch& cur = vb[b % 2];
+            cur.first = b * G;
+            cur.nv = std::min(G, n_views - b * G);
+            st = issue_views(c, s, cams, cfg, out_rgb, out_t, dev_out, counters != nullptr, b % 2, cur, &k1_ms);
+        }
+        if (st == PS_OK && b > 0)
+            st = finish_views(c, s, cams, cfg, out_rgb, out_t, dev_out, counters, (b - 1) % 2, vb[(b - 1) % 2],
+                              total);
+    }
+    if (st != PS_OK) {
+        for (ps_ctx* v : c->views) cudaStreamSynchronize(v->stream); // leave no batch in flight
+        return st;
+    }
+    // per-call totals over the views (stage times: K1 per batch on this
+    // stream, the rest summed over the views' streams, which overlap)
+    total.stage_ms[PS_STAGE_PREPROCESS] = k1_ms;
+    c->stats = total;
     return PS_OK;
 }
 

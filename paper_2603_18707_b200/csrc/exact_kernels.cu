@@ -401,20 +401,21 @@ __device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double&
     return 1;
 }
 
+// K1a for one view: splat i (in = i < n) with its camera-independent inputs
+// (mean, 3D covariance, opacity) already in registers. Every thread of the CTA
+// calls it (block-level tile aggregation inside).
 template <int BC>
-__global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
+                                              double opacity, const FrameParams& P, const FrameDev& f,
+                                              DevCounters* ctr) {
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
     bool small = false;
     unsigned long long my_mask = 0ull;
     int my_r[4] = {0, 0, -1, -1};
-    if (i < s.n) {
+    if (in) {
         unsigned long long key = ~0ull;
         uint32_t cnt = 0;
-        const double mean[3] = {s.mean[0][i], s.mean[1][i], s.mean[2][i]};
-        const double c6[6] = {s.cov[0][i], s.cov[1][i], s.cov[2][i], s.cov[3][i], s.cov[4][i], s.cov[5][i]};
-        const double opacity = s.opacity[i];
         Projected pr;
         const int st = project(mean, c6, opacity, P.cam, P.cfg.v_dilation, pr);
         if (st < 0) {
@@ -519,22 +520,55 @@ __global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, 
     }
 }
 
-template <int BK>
-__global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameDev f, double3 campos) {
+template <int BC>
+__global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= s.n || f.key[i] == ~0ull) return;
+    const bool in = i < s.n;
+    double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
+    if (in) {
+        for (int k = 0; k < 3; ++k) mean[k] = s.mean[k][i];
+        for (int k = 0; k < 6; ++k) c6[k] = s.cov[k][i];
+        opacity = s.opacity[i];
+    }
+    geometry_view<BC>(i, in, mean, c6, opacity, P, f, ctr);
+}
+
+// Multi-view K1a: each splat's camera-independent inputs are
+// read once and projected into NV views (a batch of ps_render_views), each view
+// writing its own frame arrays and counters.
+template <int NV>
+struct MultiView {
+    FrameParams P[NV];
+    FrameDev f[NV];
+    DevCounters* ctr[NV];
+};
+
+template <int BC, int NV>
+__global__ void __launch_bounds__(256, 3) k_geometry_mv(SceneDev s, MultiView<NV> mv) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = i < s.n;
+    double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
+    if (in) {
+        for (int k = 0; k < 3; ++k) mean[k] = s.mean[k][i];
+        for (int k = 0; k < 6; ++k) c6[k] = s.cov[k][i];
+        opacity = s.opacity[i];
+    }
+#pragma unroll 1
+    for (int v = 0; v < NV; ++v) geometry_view<BC>(i, in, mean, c6, opacity, mv.P[v], mv.f[v], mv.ctr[v]);
+}
+
+// K1b for one view: SH colour from the splat's coefficients (in registers) and
+// the fp32 blend record of a visible splat.
+template <int BK>
+__device__ __forceinline__ void shade_view(int64_t i, const double (&mean)[3], const float (&v)[48],
+                                           const FrameParams& P, const FrameDev& f) {
+    if (f.key[i] == ~0ull) return;
     // view direction (mean - camera position), normalised; fp32 suffices for colour
-    const float dx = static_cast<float>(s.mean[0][i] - campos.x);
-    const float dy = static_cast<float>(s.mean[1][i] - campos.y);
-    const float dz = static_cast<float>(s.mean[2][i] - campos.z);
+    const float dx = static_cast<float>(mean[0] - P.campos[0]);
+    const float dy = static_cast<float>(mean[1] - P.campos[1]);
+    const float dz = static_cast<float>(mean[2] - P.campos[2]);
     const float nrm = sqrtf(dx * dx + dy * dy + dz * dz);
     const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
-    float v[48];
-#pragma unroll
-    for (int j = 0; j < kShPlanes; ++j) {
-        const float4 t = j < P.sh_floats4 ? s.sh4[j * s.n + i] : make_float4(0.f, 0.f, 0.f, 0.f); // plane-major: coalesced
-        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
-    }
     float col[3];
     sh_color(v, P.cfg.sh_degree, dx * inv, dy * inv, dz * inv, col);
     if (P.cfg.clamp_before_blend) {
@@ -550,7 +584,42 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
     f.bl0[i] = r0;
     f.bl1[i] = r1;
     f.bl2[i] = r2;
-    (void)0;
+}
+
+template <int NVS>
+__device__ __forceinline__ void load_sh(const SceneDev& s, int64_t i, int sh_floats4, float (&v)[48]) {
+#pragma unroll
+    for (int j = 0; j < kShPlanes; ++j) {
+        const float4 t = j < sh_floats4 ? s.sh4[j * s.n + i] : make_float4(0.f, 0.f, 0.f, 0.f); // plane-major: coalesced
+        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
+    }
+}
+
+template <int BK>
+__global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameDev f) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s.n || f.key[i] == ~0ull) return;
+    const double mean[3] = {s.mean[0][i], s.mean[1][i], s.mean[2][i]};
+    float v[48];
+    load_sh<1>(s, i, P.sh_floats4, v);
+    shade_view<BK>(i, mean, v, P, f);
+}
+
+// Multi-view K1b: the splat's SH coefficients (192 B, most of K1b's traffic)
+// are read once for all NV views.
+template <int BK, int NV>
+__global__ void __launch_bounds__(256) k_shade_mv(SceneDev s, MultiView<NV> mv) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s.n) return;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) any |= mv.f[k].key[i] != ~0ull;
+    if (!any) return;
+    const double mean[3] = {s.mean[0][i], s.mean[1][i], s.mean[2][i]};
+    float v[48];
+    load_sh<NV>(s, i, mv.P[0].sh_floats4, v);
+#pragma unroll 1
+    for (int k = 0; k < NV; ++k) shade_view<BK>(i, mean, v, mv.P[k], mv.f[k]);
 }
 
 // ------------------------------------------------------------ K3 duplicate
@@ -772,14 +841,51 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
         case kBcOaP3: k_geometry<kBcOaP3><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
         default: k_geometry<kBcGeneric><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
     }
-    const double3 cp = make_double3(P.campos[0], P.campos[1], P.campos[2]);
     switch (P.blend_class) {
-        case kBkExp: k_shade<kBkExp><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
-        case kBkP1: k_shade<kBkP1><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
-        case kBkP2: k_shade<kBkP2><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
-        case kBkP3: k_shade<kBkP3><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
-        default: k_shade<kBkGeneric><<<blocks, 256, 0, st>>>(s, P, f, cp); break;
+        case kBkExp: k_shade<kBkExp><<<blocks, 256, 0, st>>>(s, P, f); break;
+        case kBkP1: k_shade<kBkP1><<<blocks, 256, 0, st>>>(s, P, f); break;
+        case kBkP2: k_shade<kBkP2><<<blocks, 256, 0, st>>>(s, P, f); break;
+        case kBkP3: k_shade<kBkP3><<<blocks, 256, 0, st>>>(s, P, f); break;
+        default: k_shade<kBkGeneric><<<blocks, 256, 0, st>>>(s, P, f); break;
     }
+}
+
+namespace {
+template <int NV>
+void launch_mv(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCounters* const* ctr, cudaStream_t st) {
+    MultiView<NV> mv;
+    for (int k = 0; k < NV; ++k) {
+        mv.P[k] = P[k];
+        mv.f[k] = f[k];
+        mv.ctr[k] = ctr[k];
+    }
+    const int blocks = static_cast<int>((s.n + 255) / 256);
+    switch (P[0].bound_class) {
+        case kBcStp: k_geometry_mv<kBcStp, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBcZero: k_geometry_mv<kBcZero, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBcOaExp: k_geometry_mv<kBcOaExp, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBcOaP1: k_geometry_mv<kBcOaP1, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBcOaP2: k_geometry_mv<kBcOaP2, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBcOaP3: k_geometry_mv<kBcOaP3, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        default: k_geometry_mv<kBcGeneric, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+    }
+    switch (P[0].blend_class) {
+        case kBkExp: k_shade_mv<kBkExp, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBkP1: k_shade_mv<kBkP1, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBkP2: k_shade_mv<kBkP2, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        case kBkP3: k_shade_mv<kBkP3, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+        default: k_shade_mv<kBkGeneric, NV><<<blocks, 256, 0, st>>>(s, mv); break;
+    }
+}
+} // namespace
+
+void launch_preprocess_views(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCounters* const* ctr,
+                             int nv, cudaStream_t st) {
+    if (s.n == 0 || nv <= 0) return;
+    if (nv == 1) launch_preprocess(s, P[0], f[0], ctr[0], st);
+    else if (nv == 2) launch_mv<2>(s, P, f, ctr, st);
+    else if (nv == 3) launch_mv<3>(s, P, f, ctr, st);
+    else launch_mv<kMaxFusedViews>(s, P, f, ctr, st);
 }
 
 void launch_scene_cov(const SceneDev& s, cudaStream_t st) {

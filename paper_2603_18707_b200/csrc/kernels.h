@@ -18,6 +18,11 @@ constexpr uint32_t kBlendSortCap = 2048u;
 // exact_kernels.cu (-fmad=false)
 void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
                        cudaStream_t st);
+// K1 fused over a batch of 1 <= nv <= kMaxFusedViews views of one scene and
+// config (same bound / blend classes): each splat's inputs read once.
+constexpr int kMaxFusedViews = 4;
+void launch_preprocess_views(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCounters* const* ctr,
+                             int nv, cudaStream_t st);
 // camera-independent 3D covariance of every splat (after each upload)
 void launch_scene_cov(const SceneDev& s, cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
