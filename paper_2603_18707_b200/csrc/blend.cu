@@ -246,8 +246,7 @@ __global__ void k_blend(const BlendArgs A) {
 constexpr int kB16 = 128;
 constexpr float kNaNf = __builtin_nanf("");
 // byte offsets of the record planes a, b, c, d in the staging area
-// (planes of kB16 + 1 records: slot kB16 is the null record, never accepted)
-constexpr int kRecs = kB16 + 1;
+constexpr int kRecs = kB16;
 constexpr uint32_t kOffB = kRecs * 16, kOffC = 2 * kRecs * 16, kOffD = 3 * kRecs * 16;
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
@@ -377,8 +376,7 @@ struct Pair {
 };
 
 // One record's fragments for both pixels of a pair: everything that does not
-// depend on the pixels' running state (so two records' fragments can be
-// computed back to back and their latencies overlap).
+// depend on the pixels' running state (alpha, the skip / ambiguity decisions).
 struct Frag {
     float n0, n1;          // -alpha (0 when skipped)
     float g0, g1;          // g' (0 when skipped)
@@ -462,7 +460,7 @@ __device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const Fr
 }
 
 // Blends fragment f (list position jpos) into the pair. When a pixel finishes
-// here, `next` (the following record's fragments, already computed) is
+// here, `next` (a following record's fragments, if already computed) is
 // cancelled for it; m (the pair's remaining candidates) is cleared when both
 // pixels are finished.
 template <bool COUNT>
@@ -634,7 +632,6 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     float4* sD = sA + 3 * kRecs;
     uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kRecs); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
-    const uint32_t s_null = s_rec + kB16 * 16u;
 
     if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
     const FrameParams& P = A.P;
@@ -693,12 +690,6 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             sB[t] = make_float4(gamma, qhi, pb1.x, gp);
             sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
             sD[t] = make_float4(-K1, -K2, -K3, 0.f);
-            if (t == 0) { // null record: q = dy^2 > q_hi = -1 (alpha mode: alpha 0 < eps + 1)
-                sA[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
-                sB[kB16] = make_float4(1.f, -1.f, 3.0e38f, 0.f);
-                sC[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
-                sD[kB16] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
             // coverage of {q <= q_hi}: word w = 8 rows x 4 pairs of warp w's block
             uint32_t cw[4] = {0u, 0u, 0u, 0u};
             const bool full = MODE != kQuadricThreshold || !(qhi < 3.0e38f) || !(Aq > 0.0f) ||
@@ -744,19 +735,11 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             const uint32_t rb = s_rec + static_cast<uint32_t>(k0) * 16u;
             const int jb = base + k0;
             if (!((f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x)))) m = 0u; // both finished
-            // two candidates per iteration (the second one the null record
-            // when only one is left): both records' fragments first, so their
-            // loads and arithmetic overlap, then the two blends in list order
             while (m != 0u) {
-                const uint32_t j1 = static_cast<uint32_t>(__ffs(m) - 1);
+                const uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
                 m &= m - 1u;
-                const uint32_t j2 = m ? static_cast<uint32_t>(__ffs(m) - 1) : j1;
-                const uint32_t r2 = m ? rb + j2 * 16u : s_null;
-                m &= m - 1u;
-                const Frag f1 = pair_frag<KIND, ORDER, MODE>(p.x, rb + j1 * 16u, yc, P);
-                Frag f2_ = pair_frag<KIND, ORDER, MODE>(p.x, r2, yc, P);
-                pair_blend<COUNT>(p, f1, jb + static_cast<int>(j1), P, m, &f2_);
-                pair_blend<COUNT>(p, f2_, jb + static_cast<int>(j2), P, m, nullptr);
+                const Frag fr = pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P);
+                pair_blend<COUNT>(p, fr, jb + static_cast<int>(j), P, m, nullptr);
             }
         }
     }

@@ -17,7 +17,7 @@ def find(pat, start=0):
 
 k = find(r"__global__ void __launch_bounds__\(128, 6\) k_blend16")
 ranges = {
-    "walk": (find(r"__device__ __forceinline__ void pair_step"), find(r"^// alpha of \(pixel")),
+    "walk": (find(r"^struct Frag \{"), find(r"^// alpha of \(pixel")),
     "stage+cover": (find(r"stage the record prefetched", k), find(r"prefetch the next batch", k)),
     "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Shared-memory record")),
     "transpose": (find(r"warp_transpose32\(uint32_t x"), find(r"^// ---- packed fp32 pairs")),
