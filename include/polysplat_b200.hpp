@@ -21,8 +21,10 @@
 #include <vector>
 
 #include "polysplat/errors.hpp"
+#include "polysplat/metrics.hpp"
 #include "polysplat/projection.hpp"
 #include "polysplat/raster.hpp"
+#include "polysplat/scene_io.hpp"
 #include "polysplat_b200.h"
 
 namespace polysplat::b200 {
@@ -40,6 +42,11 @@ static_assert(sizeof(Splat3D) == PS_SPLAT3D_DOUBLES * sizeof(double), "Splat3D l
         case PS_EPSILON_ZERO_UNBOUNDED: throw EpsilonZeroUnbounded(m);
         case PS_FULLY_CULLED: throw FullyCulled(m);
         case PS_ERROR: throw Error(m);
+        case PS_IO_ERROR: throw IoError(m);
+        case PS_MALFORMED_HEADER: throw MalformedHeader(m);
+        case PS_UNSUPPORTED_FORMAT: throw UnsupportedFormat(m);
+        case PS_MISSING_PROPERTY: throw MissingProperty(m);
+        case PS_TRUNCATED_DATA: throw TruncatedData(m);
         default: throw std::runtime_error(m);
     }
 }
@@ -219,6 +226,79 @@ inline std::vector<ProjectedSplat> prepare_splats(std::span<const Splat3D> splat
         p.index = index[k];
     }
     return res;
+}
+
+// Many views of one resident scene (K1 fused over batches of views; each
+// view's binning / blend on its own stream). All cameras share width / height.
+inline std::vector<std::pair<Framebuffer, PerfCounters>> render_views(const Scene& scene,
+                                                                      std::span<const Camera> cams,
+                                                                      const RasterConfig& cfg) {
+    std::vector<std::pair<Framebuffer, PerfCounters>> out;
+    if (cams.empty()) return out;
+    std::vector<ps_camera> c(cams.size());
+    for (std::size_t k = 0; k < cams.size(); ++k) c[k] = to_ps(cams[k]);
+    const ps_config g = to_ps(cfg);
+    const std::size_t pix = static_cast<std::size_t>(cams[0].width) * cams[0].height;
+    std::vector<float> rgb(3 * pix * cams.size()), tr(pix * cams.size());
+    std::vector<ps_counters> ctr(cams.size());
+    scene.device().check(ps_render_views(scene.device().get(), scene.get(), c.data(), static_cast<int>(c.size()), &g,
+                                         rgb.data(), tr.data(), PS_MEM_HOST, ctr.data()));
+    for (std::size_t v = 0; v < cams.size(); ++v) {
+        Framebuffer fb(cams[v].width, cams[v].height);
+        for (std::size_t k = 0; k < 3 * pix; ++k) fb.rgb[k] = rgb[3 * pix * v + k];
+        for (std::size_t k = 0; k < pix; ++k) fb.transmittance[k] = tr[pix * v + k];
+        out.emplace_back(std::move(fb), from_ps(ctr[v]));
+    }
+    return out;
+}
+
+// polysplat::compare (metrics.hpp:40-42): both configs rendered and compared
+// on the device (composite, psnr, ssim, max_abs_diff; counters; pair ratio).
+inline CompareReport compare(std::span<const Splat3D> splats, const Camera& cam, const RasterConfig& cfg_a,
+                             const RasterConfig& cfg_b, const Vec3& background = {1.0, 1.0, 1.0},
+                             Device& dev = default_device()) {
+    Scene s(dev, splats);
+    const ps_camera c = to_ps(cam);
+    const ps_config ga = to_ps(cfg_a), gb = to_ps(cfg_b);
+    const double bg[3] = {background.x, background.y, background.z};
+    ps_compare_report r;
+    dev.check(ps_compare(dev.get(), s.get(), &c, &ga, &gb, bg, &r));
+    if (!r.metrics.ssim_valid) throw TooSmall("ssim needs images at least 11x11");
+    CompareReport out;
+    out.psnr_db = r.metrics.psnr_db;
+    out.ssim = r.metrics.ssim;
+    out.max_abs_diff = r.metrics.max_abs_diff;
+    out.counters_a = from_ps(r.counters_a);
+    out.counters_b = from_ps(r.counters_b);
+    out.pair_ratio = r.pair_ratio;
+    return out;
+}
+
+// psnr / ssim / max_abs_diff of two framebuffers on the device (composite +
+// metrics.cpp:34-134), in one pass.
+inline ps_image_metrics image_metrics(const Framebuffer& a, const Framebuffer& b,
+                                      const Vec3& background = {1.0, 1.0, 1.0}, Device& dev = default_device()) {
+    if (a.width != b.width || a.height != b.height) throw DimensionMismatch("image dimensions differ");
+    const double bg[3] = {background.x, background.y, background.z};
+    ps_image_metrics m;
+    dev.check(ps_image_metrics_compute(dev.get(), a.width, a.height, a.rgb.data(), a.transmittance.data(),
+                                       b.rgb.data(), b.transmittance.data(), PS_DTYPE_F64, PS_MEM_HOST, bg, &m));
+    return m;
+}
+
+// polysplat::load_ply (scene_io.hpp:23-27): same fields to the bit, same errors.
+inline SceneFile load_ply(const std::string& path) {
+    int64_t n = 0;
+    int deg = 0;
+    int st = ps_ply_info(path.c_str(), &n, &deg);
+    if (st != PS_OK) throw_status(st, ps_last_error(nullptr));
+    SceneFile sf;
+    sf.source_path = path;
+    sf.splats.resize(static_cast<std::size_t>(n));
+    st = ps_ply_load_splat3d(path.c_str(), reinterpret_cast<double*>(sf.splats.data()), n, &n, &deg);
+    if (st != PS_OK) throw_status(st, ps_last_error(nullptr));
+    sf.sh_degree = deg;
+    return sf;
 }
 
 } // namespace polysplat::b200

@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "polysplat/kernel.hpp"
+#include "polysplat/metrics.hpp"
 #include "polysplat/raster.hpp"
 #include "polysplat/scene_io.hpp"
 #include "polysplat_b200.hpp"
@@ -65,6 +66,36 @@ int main() {
                      std::fabs(a[k].bound.quadric_root - b[k].bound.quadric_root) <= 1e-13 * a[k].bound.quadric_root;
             std::snprintf(buf, sizeof buf, "prepare_splats scene %d %s (%zu)", si, c.name, a.size());
             check(eq, buf);
+        }
+    }
+    // compare (metrics.cpp:138-157): same counters; quality within the 1e-5 image tolerance
+    {
+        RasterConfig ca, cb;
+        ca.sh_degree = cb.sh_degree = scenes[1].sh_degree;
+        cb.kernel = poly1;
+        cb.culling_mode = CullingMode::OpacityAware;
+        CompareReport r = polysplat::compare(scenes[1].splats, cams[1], ca, cb);
+        CompareReport g = polysplat::b200::compare(scenes[1].splats, cams[1], ca, cb);
+        const bool ok = r.counters_b.tile_pairs_after_tight_test == g.counters_b.tile_pairs_after_tight_test &&
+                        r.pair_ratio == g.pair_ratio && std::fabs(r.psnr_db - g.psnr_db) < 1e-2 &&
+                        std::fabs(r.ssim - g.ssim) < 1e-4 && std::fabs(r.max_abs_diff - g.max_abs_diff) <= 2e-5;
+        std::snprintf(buf, sizeof buf, "compare: psnr %.6f vs %.6f, ssim %.6f vs %.6f", r.psnr_db, g.psnr_db, r.ssim,
+                      g.ssim);
+        check(ok, buf);
+    }
+    // load_ply (scene_io.cpp:53-199): the reference's writer, both loaders, bitwise
+    {
+        const char* path = "/tmp/adapter_parity.ply";
+        write_ply(scenes[1], path);
+        SceneFile a = polysplat::load_ply(path), b = polysplat::b200::load_ply(path);
+        const bool ok = a.sh_degree == b.sh_degree && a.splats.size() == b.splats.size() &&
+                        std::memcmp(a.splats.data(), b.splats.data(), sizeof(Splat3D) * a.splats.size()) == 0;
+        check(ok, "load_ply bitwise");
+        try {
+            polysplat::b200::load_ply("/nonexistent/x.ply");
+            check(false, "missing file throws IoError");
+        } catch (const IoError&) {
+            check(true, "missing file throws IoError");
         }
     }
     // error convention: invalid config -> std::invalid_argument
