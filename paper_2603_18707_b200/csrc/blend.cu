@@ -288,46 +288,17 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
     return x;
 }
 
-// ---- packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2; scalars broadcast as .F32 operands)
-struct F2 {
-    unsigned long long v;
-};
-__device__ __forceinline__ F2 f2(float lo, float hi) {
-    F2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ F2 f2b(float s) { return f2(s, s); }
-__device__ __forceinline__ float f2lo(F2 a) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
-    return lo;
-}
-__device__ __forceinline__ float f2hi(F2 a) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
-    return hi;
-}
-__device__ __forceinline__ F2 f2add(F2 a, F2 b) {
-    F2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2sub(F2 a, F2 b) {
-    F2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2mul(F2 a, F2 b) {
-    F2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2fma(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
+// ---- packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2 via the CUDA builtins;
+// a broadcast scalar becomes a .F32 operand, a negation an operand modifier)
+using F2 = float2;
+__device__ __forceinline__ F2 f2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ F2 f2b(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float f2lo(F2 a) { return a.x; }
+__device__ __forceinline__ float f2hi(F2 a) { return a.y; }
+__device__ __forceinline__ F2 f2add(F2 a, F2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ F2 f2sub(F2 a, F2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ F2 f2mul(F2 a, F2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ F2 f2fma(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 
 // Conservative coverage of {q <= q_hi} over the 16 pixel centres of tile row
 // `row`, widened to the row's 8 pixel pairs (bit k = pair (2k, 2k+1)). Every
@@ -355,18 +326,19 @@ __device__ __forceinline__ uint32_t row_pairs(int row, float mx, float my, float
 // in alpha-threshold mode). The walk carries NEGATED alphas (-alpha = Horner
 // over the negated coefficients, exactly), so that T' = fma(-alpha, T, T) is
 // one rounding and the colour update fma(-alpha T, -c, rgb) needs no negation.
-// g' = 1.001 (g + 2.2u) + 4u64 widens g = the splat's |alpha_fp32 - alpha_ref|
+// g' = 1.001 (g + 3.2u) + 4u64 widens g = the splat's |alpha_fp32 - alpha_ref|
 // bound (u = 2^-24, u64 = 2^-53) for the interval update below.
 //
 // Per-pair state of the walk. Invariant: for each live pixel, the reference's
 // fp64 transmittance lies in [Lo, Up]. A blend of a fragment with fp32 alpha a
 // (so alpha_ref in [a - g, a + g]) maps it to
-//     Up' = fma(Up, g', fma(-a, Up, Up)),   Lo' = fma(Lo, -g', fma(-a, Lo, Lo))
-// (each inner fma is Up (1 - a) with one rounding; g' covers both fp32
-// roundings and the reference's two fp64 roundings), so the reference's
-// test_t < floor is certainly false when Lo' >= floor and certainly true when
-// Up' < floor; only the band between is undecided (exact replay). T itself is
-// the fp32 value blended with (T' = fma(-a, T, T)).
+//     Up' = fma(Up, (-a) + g', Up),   Lo' = fma(Lo, (-a) - g', Lo)
+// The sum (-a) +- g' is rounded once (absolute error <= u, as |a| + g' < 1) and
+// the fma once (relative u of a result >= Up (1 - a)); g' - g covers both, and
+// the reference's two fp64 roundings, so the reference's test_t < floor is
+// certainly false when Lo' >= floor and certainly true when Up' < floor; only
+// the band between is undecided (exact replay). T itself is the fp32 value
+// blended with (T' = fma(-a, T, T)).
 struct Pair {
     F2 x;                   // tile-local pixel-centre x of both pixels (NaN once finished)
     F2 T, Up, Lo, r, g, b;
@@ -468,9 +440,8 @@ __device__ __forceinline__ void pair_blend(Pair& p, Frag f, int jpos, const Fram
                                            Frag* next) {
     F2 na = f2(f.n0, f.n1);
     const F2 gp = f2(f.g0, f.g1);
-    F2 tt = f2fma(na, p.T, p.T); // T (1 - alpha), one rounding; == T when skipped
-    const F2 up = f2fma(p.Up, gp, f2fma(na, p.Up, p.Up));
-    F2 lo = f2fma(p.Lo, f2mul(gp, f2b(-1.0f)), f2fma(na, p.Lo, p.Lo));
+    const F2 up = f2fma(p.Up, f2add(na, gp), p.Up);
+    F2 lo = f2fma(p.Lo, f2sub(na, gp), p.Lo);
     // Transmittance decision (raster.cpp:272-277): the reference terminates iff
     // its test_t < floor; Lo' >= floor certifies it does not (the common case,
     // no branch); otherwise decide per pixel below.
@@ -501,15 +472,14 @@ __device__ __forceinline__ void pair_blend(Pair& p, Frag f, int jpos, const Fram
         }
         p.x = f2(x0, x1);
         na = f2(f.n0, f.n1);
-        tt = f2fma(na, p.T, p.T);
         lo = f2(l0, l1);
         if (x0 != x0 && x1 != x1) m = 0u; // both pixels finished
     }
-    const F2 w = f2mul(na, p.T); // -alpha T
+    const F2 w = f2mul(na, p.T);  // -alpha T
+    p.T = f2fma(na, p.T, p.T);    // T (1 - alpha), one rounding; == T when skipped or finished
     p.r = f2fma(w, f2b(f.cr), p.r);
     p.g = f2fma(w, f2b(f.cg), p.g);
     p.b = f2fma(w, f2b(f.cb), p.b);
-    p.T = tt;
     p.Up = up;
     p.Lo = lo;
     if (COUNT) {
@@ -685,7 +655,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             if (KIND == 1 && MODE == kQuadricThreshold) {
                 K0 = o * c0; K1 = o * c1; K2 = o * c2; K3 = o * c3;
             }
-            const float gp = fmaf(1.001f, fmaf(2.2f, 5.9604645e-08f, ga), 4.5e-16f);
+            const float gp = fmaf(1.001f, fmaf(3.2f, 5.9604645e-08f, ga), 4.5e-16f);
             sA[t] = make_float4(mx, my, Aq, beta);
             sB[t] = make_float4(gamma, qhi, pb1.x, gp);
             sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
@@ -735,11 +705,18 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             const uint32_t rb = s_rec + static_cast<uint32_t>(k0) * 16u;
             const int jb = base + k0;
             if (!((f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x)))) m = 0u; // both finished
+            // unrolled by two so the loop-carried pair state alternates
+            // between two register sets instead of being copied every step
             while (m != 0u) {
-                const uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
+                uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
                 m &= m - 1u;
-                const Frag fr = pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P);
-                pair_blend<COUNT>(p, fr, jb + static_cast<int>(j), P, m, nullptr);
+                pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
+                                  P, m, nullptr);
+                if (m == 0u) break;
+                j = static_cast<uint32_t>(__ffs(m) - 1);
+                m &= m - 1u;
+                pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
+                                  P, m, nullptr);
             }
         }
     }
