@@ -358,8 +358,9 @@ struct Frag {
 };
 
 // Fragments of the record staged at shared address rec for the pair's pixels
-// (x = their tile-local centres) at row centre yc.
-template <int KIND, int ORDER, int MODE>
+// (x = their tile-local centres) at row centre yc. CLAMP: apply min(.999, .)
+// (quadric mode skips it for batches whose records cannot reach .999).
+template <int KIND, int ORDER, int MODE, bool CLAMP>
 __device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const FrameParams& P) {
     const float4 a = lds128(rec);
     const float4 b = lds128(rec + kOffB);
@@ -394,8 +395,8 @@ __device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const Fr
             pq = f2fma(pq, q, f2b(d.x));
             na = f2fma(pq, q, f2b(c.x));
         }
-        f.n0 = fmaxf(-0.999f, f2lo(na));
-        f.n1 = fmaxf(-0.999f, f2hi(na));
+        f.n0 = CLAMP ? fmaxf(-0.999f, f2lo(na)) : f2lo(na);
+        f.n1 = CLAMP ? fmaxf(-0.999f, f2hi(na)) : f2hi(na);
     } else {
         // non-monotone kernel: full ReLU / piecewise semantics, guard on alpha
         const KernelF32& kf = P.kf;
@@ -485,6 +486,24 @@ __device__ __forceinline__ void pair_blend(Pair& p, Frag f, int jpos, const Fram
     if (COUNT) {
         p.nbl0 += f.skip0 ? 0u : 1u;
         p.nbl1 += f.skip1 ? 0u : 1u;
+    }
+}
+
+// One warp's walk over a group's candidate mask m (records at shared address
+// rb, list positions jb + bit). Unrolled by two so the loop-carried pair state
+// alternates between two register sets instead of being copied every step.
+template <int KIND, int ORDER, int MODE, bool COUNT, bool CLAMP>
+__device__ __forceinline__ void walk(Pair& p, uint32_t m, uint32_t rb, float yc, const FrameParams& P, int jb) {
+    while (m != 0u) {
+        uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
+        m &= m - 1u;
+        pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE, CLAMP>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
+                          P, m, nullptr);
+        if (m == 0u) break;
+        j = static_cast<uint32_t>(__ffs(m) - 1);
+        m &= m - 1u;
+        pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE, CLAMP>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
+                          P, m, nullptr);
     }
 }
 
@@ -647,6 +666,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
     for (int base = 0; base < L; base += kB16) {
         const bool live = (f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x));
         if (__syncthreads_count(live) == 0) break;
+        bool needs_clamp;
         {   // stage the record prefetched for this batch
             const float mx = static_cast<float>(pm.x - px0), my = static_cast<float>(pm.y - py0);
             const float Aq = pb0.x, beta = pb0.y, gamma = pb0.z, qhi = pb0.w;
@@ -656,6 +676,10 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
                 K0 = o * c0; K1 = o * c1; K2 = o * c2; K3 = o * c3;
             }
             const float gp = fmaf(1.001f, fmaf(3.2f, 5.9604645e-08f, ga), 4.5e-16f);
+            // can this record's alpha reach the .999 clamp? (quadric mode: the
+            // kernel is non-increasing in q >= 0, so alpha <= alpha(0) = K0, resp.
+            // 2^K0 = o for exp; the margin covers fp32 Horner rounding)
+            needs_clamp = t < L - base && (MODE != kQuadricThreshold || (KIND == 0 ? pb1.y >= -1.6e-3f : K0 >= 0.9989f));
             sA[t] = make_float4(mx, my, Aq, beta);
             sB[t] = make_float4(gamma, qhi, pb1.x, gp);
             sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
@@ -683,7 +707,7 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) cover[j][t] = cw[j];
         }
-        __syncthreads();
+        const bool clamp = __syncthreads_or(needs_clamp) != 0;
         const int nb = base + kB16;
         if (nb + t < L) { // prefetch the next batch while this one is blended
             const uint32_t pi = list[nb + t];
@@ -705,19 +729,8 @@ __global__ void __launch_bounds__(128, 6) k_blend16(const BlendArgs A) {
             const uint32_t rb = s_rec + static_cast<uint32_t>(k0) * 16u;
             const int jb = base + k0;
             if (!((f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x)))) m = 0u; // both finished
-            // unrolled by two so the loop-carried pair state alternates
-            // between two register sets instead of being copied every step
-            while (m != 0u) {
-                uint32_t j = static_cast<uint32_t>(__ffs(m) - 1);
-                m &= m - 1u;
-                pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
-                                  P, m, nullptr);
-                if (m == 0u) break;
-                j = static_cast<uint32_t>(__ffs(m) - 1);
-                m &= m - 1u;
-                pair_blend<COUNT>(p, pair_frag<KIND, ORDER, MODE>(p.x, rb + j * 16u, yc, P), jb + static_cast<int>(j),
-                                  P, m, nullptr);
-            }
+            if (clamp) walk<KIND, ORDER, MODE, COUNT, true>(p, m, rb, yc, P, jb);
+            else walk<KIND, ORDER, MODE, COUNT, false>(p, m, rb, yc, P, jb);
         }
     }
 

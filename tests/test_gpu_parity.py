@@ -108,3 +108,26 @@ def test_cpp_adapter_dropin_parity(gpu):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.parametrize("kname", ["steep_poly1", "exp"])
+def test_alpha_clamp_active(gpu, reference, kname):
+    """Splats whose alpha reaches the reference's min(0.999, .) clamp
+    (raster.cpp:267): opacity ~1 with a poly-1 kernel of c0 = 1.2 (alpha 1.2
+    at the centre) or the exponential; the blend applies the clamp only in
+    batches that need it."""
+    splats, deg = scene("g", 1, 10000)
+    splats = splats.copy()
+    rng = np.random.default_rng(7)
+    hi = rng.uniform(0, 1, len(splats)) < 0.3
+    splats[hi, 10] = 1.0  # opacity column of Splat3D
+    if kname == "exp":
+        cfg = config("exp", api.CullingMode.StopThePop, deg)
+    else:
+        k = api.make_polynomial_kernel(api.KernelKind.PolynomialRelu, (1.2, -0.3))
+        cfg = api.RasterConfig(kernel=k, culling_mode=api.CullingMode.OpacityAware, sh_degree=deg)
+    cam = camera(1, 256, 256, 0)
+    rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+    fb, ctr = gpu.render(splats, cam, cfg)
+    assert ctr.as_dict() == ctr_r
+    assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
