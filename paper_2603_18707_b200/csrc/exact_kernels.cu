@@ -677,18 +677,24 @@ __global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameP
     __shared__ int wb[4];
     if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool active = i < n && f.tcount[i] != 0;
+    // all of a splat's inputs are loaded at once (one memory round trip; the
+    // rect / mask / key of an inactive splat are stale and unused)
+    const int64_t ic = i < n ? i : 0;
+    const uint32_t tc = f.tcount[ic];
+    const ushort4 rc = f.rect[ic];
+    const unsigned long long tm = f.tmask[ic];
+    const unsigned long long kk = f.key[ic];
+    const bool active = i < n && tc != 0;
     int r[4] = {0, 0, -1, -1};
     unsigned long long m0 = 0ull;
     bool small = false;
     uint32_t k32 = 0u; // coarse depth key stored next to every bucket entry (tile_sort.cuh)
     if (active) {
-        k32 = coarse_key(f.key[i], ~ctr->key_min, ctr->key_max);
-        const ushort4 rc = f.rect[i];
+        k32 = coarse_key(kk, ~ctr->key_min, ctr->key_max);
         r[0] = rc.x; r[1] = rc.y; r[2] = rc.z; r[3] = rc.w;
         if (rect_is_small(r)) {
             small = true;
-            m0 = f.tmask[i];
+            m0 = tm;
         } else { // big rect: exact tests, direct atomics (rare)
             duplicate_big(f.pval, f.pkey, k32, f.tile_count, f.mean2d[i], f.conic_ab[i], f.conic_cq[i], P.cfg.tile_size,
                           P.tiles_x, static_cast<uint32_t>(i), r[0], r[1], r[2], r[3]);
