@@ -42,8 +42,10 @@ struct TileSortSmem {
     static constexpr int WARPS = THREADS / 32;
     static constexpr int BINS = CAP >= 8192 ? 4096 : CAP >= 2048 ? 2048 : 1024;
     static constexpr int BIN_SHIFT = 32 - ilog2_c(BINS);
-    // vin [CAP] u32 | nk [CAP] u32 | perm [CAP] u16 | dest [CAP] u16 | hist [BINS] -> sorted list [CAP]
-    static constexpr int LIST = 3 * CAP; // word offset of the sorted list
+    // nk [CAP] u32 | perm [CAP] u16 | dest [CAP] u16 | hist [BINS] -> sorted list [CAP]
+    // (the bucket's splat indices are re-read from global memory, L2-resident,
+    // rather than kept in shared memory: 12 B per slot + the list)
+    static constexpr int LIST = 2 * CAP; // word offset of the sorted list
     static constexpr size_t WORDS = LIST + (CAP > BINS ? CAP : BINS);
     __host__ __device__ static constexpr size_t bytes() { return sizeof(uint32_t) * WORDS; }
 };
@@ -59,9 +61,9 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     constexpr int CAP = S::CAP, BINS = S::BINS, WARPS = S::WARPS, SH = S::BIN_SHIFT;
     constexpr int PER = BINS / THREADS;
     static_assert(BINS % (4 * THREADS) == 0 && CAP <= 65536, "tile sort shape");
-    uint32_t* vin = smem;                                             // bucket order
-    uint32_t* nk = smem + CAP;                                        // 32-bit key per bucket slot
-    uint16_t* perm = reinterpret_cast<uint16_t*>(smem + 2 * CAP);      // bin-sorted position -> slot
+    const uint32_t* vin = pval + r.x;                                 // bucket order (global)
+    uint32_t* nk = smem;                                              // 32-bit key per bucket slot
+    uint16_t* perm = reinterpret_cast<uint16_t*>(smem + CAP);          // bin-sorted position -> slot
     uint16_t* dest = perm + CAP;                                       // bin-sorted position -> final
     uint32_t* hist = smem + S::LIST;                                  // counts -> cursors -> list
     __shared__ uint32_t red_min[WARPS], red_max[WARPS];
@@ -73,7 +75,6 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     uint32_t lo = 0xffffffffu, hi = 0u;
     for (int j = t; j < L; j += THREADS) {
         const uint32_t k = pkey[r.x + j];
-        vin[j] = pval[r.x + j];
         nk[j] = k;
         lo = min(lo, k);
         hi = max(hi, k);
@@ -129,13 +130,12 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         if (e - s > kMaxRun) {
             need_bitonic = 1;
         } else if (e - s > 1) {
-            const uint32_t v = vin[j];
             for (int i = s; i < e; ++i) {
                 const uint32_t ji = perm[i];
                 const uint32_t xi = nk[ji];
                 bool before = xi < x;
                 if (xi == x && ji != j) {
-                    const uint32_t vi = vin[ji];
+                    const uint32_t v = vin[j], vi = vin[ji];
                     const unsigned long long ki = key[vi], kv = key[v];
                     before = ki < kv || (ki == kv && orig[vi] < orig[v]);
                 }
@@ -150,7 +150,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         for (int p = t; p < L; p += THREADS) list[dest[p]] = vin[perm[p]];
     } else {
         // degenerate depth clusters: exact bitonic sort on (bits, original index);
-        // full keys over the (now dead) vin / nk arrays
+        // full keys over the (now dead) nk / perm / dest arrays
         for (int p = t; p < L; p += THREADS) list[p] = vin[perm[p]];
         __syncthreads();
         unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem);
