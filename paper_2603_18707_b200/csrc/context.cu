@@ -415,8 +415,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
         if (f.tile_count) CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * n_tiles, strm));
         // K1: preprocess (+ tight pair count per tile)
-        launch_preprocess(s->dev, P, f, c->d_ctr, strm);
-        launches += n > 0 ? 2 : 0;
+        launches += launch_preprocess(s->dev, P, f, c->d_ctr, strm);
     }
     record(c, 1);
     const uint32_t* order = nullptr;

@@ -404,10 +404,17 @@ __device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double&
 // K1a for one view: splat i (in = i < n) with its camera-independent inputs
 // (mean, 3D covariance, opacity) already in registers. Every thread of the CTA
 // calls it (block-level tile aggregation inside).
+// What the shading of a visible splat needs from K1a (the fused kernel passes it
+// in registers instead of through the frame arrays).
+struct GeoOut {
+    bool visible = false;
+    double a = 0.0, b = 0.0, c = 0.0, o = 0.0; // conic (xx, xy, yy), opacity_eff
+};
+
 template <int BC>
 __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
                                               double opacity, const FrameParams& P, const FrameDev& f,
-                                              DevCounters* ctr) {
+                                              DevCounters* ctr, GeoOut* out = nullptr) {
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
     bool small = false;
@@ -460,6 +467,13 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                     f.rect[i] = make_ushort4(static_cast<unsigned short>(r[0]), static_cast<unsigned short>(r[1]),
                                              static_cast<unsigned short>(r[2]), static_cast<unsigned short>(r[3]));
                     f.opacity_eff[i] = pr.opacity_eff;
+                    if (out) {
+                        out->visible = true;
+                        out->a = pr.conic.xx;
+                        out->b = pr.conic.xy;
+                        out->c = pr.conic.yy;
+                        out->o = pr.opacity_eff;
+                    }
                     if (f.cov_aa) {
                         f.cov_aa[3 * i] = pr.cov_aa.xx;
                         f.cov_aa[3 * i + 1] = pr.cov_aa.xy;
@@ -560,9 +574,9 @@ __global__ void __launch_bounds__(256, 3) k_geometry_mv(SceneDev s, MultiView<NV
 // K1b for one view: SH colour from the splat's coefficients (in registers) and
 // the fp32 blend record of a visible splat.
 template <int BK>
-__device__ __forceinline__ void shade_view(int64_t i, const double (&mean)[3], const float (&v)[48],
-                                           const FrameParams& P, const FrameDev& f) {
-    if (f.key[i] == ~0ull) return;
+__device__ __forceinline__ void shade_record(int64_t i, const double (&mean)[3], const float (&v)[48],
+                                             const FrameParams& P, const FrameDev& f, double ca, double cb, double cc,
+                                             double o) {
     // view direction (mean - camera position), normalised; fp32 suffices for colour
     const float dx = static_cast<float>(mean[0] - P.campos[0]);
     const float dy = static_cast<float>(mean[1] - P.campos[1]);
@@ -576,14 +590,21 @@ __device__ __forceinline__ void shade_view(int64_t i, const double (&mean)[3], c
         col[1] = fminf(fmaxf(col[1], 0.f), 1.f);
         col[2] = fminf(fmaxf(col[2], 0.f), 1.f);
     }
-    const double2 ab = f.conic_ab[i];
-    const double2 cq = f.conic_cq[i];
     float4 r0, r1;
     float2 r2;
-    blend_record<BK>(ab.x, ab.y, cq.x, f.opacity_eff[i], P, col[0], col[1], col[2], r0, r1, r2);
+    blend_record<BK>(ca, cb, cc, o, P, col[0], col[1], col[2], r0, r1, r2);
     f.bl0[i] = r0;
     f.bl1[i] = r1;
     f.bl2[i] = r2;
+}
+
+template <int BK>
+__device__ __forceinline__ void shade_view(int64_t i, const double (&mean)[3], const float (&v)[48],
+                                           const FrameParams& P, const FrameDev& f) {
+    if (f.key[i] == ~0ull) return;
+    const double2 ab = f.conic_ab[i];
+    const double2 cq = f.conic_cq[i];
+    shade_record<BK>(i, mean, v, P, f, ab.x, ab.y, cq.x, f.opacity_eff[i]);
 }
 
 template <int NVS>
@@ -603,6 +624,29 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
     float v[48];
     load_sh<1>(s, i, P.sh_floats4, v);
     shade_view<BK>(i, mean, v, P, f);
+}
+
+// K1 fused (K1a + K1b in one kernel, for the common culling x blend kernel
+// pairs): the SH loads and colour of a visible splat follow its projection in
+// the same thread, so the HBM-bound SH traffic overlaps the fp64-latency-bound
+// geometry of other warps, and the conic / opacity stay in registers.
+template <int BC, int BK>
+__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = i < s.n;
+    double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
+    if (in) {
+        for (int k = 0; k < 3; ++k) mean[k] = s.mean[k][i];
+        for (int k = 0; k < 6; ++k) c6[k] = s.cov[k][i];
+        opacity = s.opacity[i];
+    }
+    GeoOut g;
+    geometry_view<BC>(i, in, mean, c6, opacity, P, f, ctr, &g);
+    if (g.visible) {
+        float v[48];
+        load_sh<1>(s, i, P.sh_floats4, v);
+        shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o);
+    }
 }
 
 // Multi-view K1b: the splat's SH coefficients (192 B, most of K1b's traffic)
@@ -834,10 +878,25 @@ __global__ void __launch_bounds__(256) k_scene_cov(SceneDev s) {
 }
 
 // ------------------------------------------------------------ launchers
-void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
-                       cudaStream_t st) {
-    if (s.n == 0) return;
+int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
+                      cudaStream_t st) {
+    if (s.n == 0) return 0;
     const int blocks = static_cast<int>((s.n + 255) / 256);
+    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323)
+#define PS_FUSED(BCV, BKV)                                                                 \
+    if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
+        k_preprocess<BCV, BKV><<<blocks, 256, 0, st>>>(s, P, f, ctr);                    \
+        return 1;                                                                        \
+    }
+    PS_FUSED(kBcStp, kBkExp)
+    PS_FUSED(kBcOaExp, kBkExp)
+    PS_FUSED(kBcStp, kBkP1)
+    PS_FUSED(kBcZero, kBkP1)
+    PS_FUSED(kBcOaP1, kBkP1)
+    PS_FUSED(kBcOaP2, kBkP2)
+    PS_FUSED(kBcStp, kBkP3)
+    PS_FUSED(kBcOaP3, kBkP3)
+#undef PS_FUSED
     switch (P.bound_class) {
         case kBcStp: k_geometry<kBcStp><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
         case kBcZero: k_geometry<kBcZero><<<blocks, 256, 0, st>>>(s, P, f, ctr); break;
@@ -854,6 +913,7 @@ void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& 
         case kBkP3: k_shade<kBkP3><<<blocks, 256, 0, st>>>(s, P, f); break;
         default: k_shade<kBkGeneric><<<blocks, 256, 0, st>>>(s, P, f); break;
     }
+    return 2;
 }
 
 namespace {
@@ -888,7 +948,7 @@ void launch_mv(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCo
 void launch_preprocess_views(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCounters* const* ctr,
                              int nv, cudaStream_t st) {
     if (s.n == 0 || nv <= 0) return;
-    if (nv == 1) launch_preprocess(s, P[0], f[0], ctr[0], st);
+    if (nv == 1) (void)launch_preprocess(s, P[0], f[0], ctr[0], st);
     else if (nv == 2) launch_mv<2>(s, P, f, ctr, st);
     else if (nv == 3) launch_mv<3>(s, P, f, ctr, st);
     else launch_mv<kMaxFusedViews>(s, P, f, ctr, st);

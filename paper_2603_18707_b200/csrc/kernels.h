@@ -16,8 +16,9 @@ constexpr uint32_t kMaxBucketSorted = 12288u;
 constexpr uint32_t kBlendSortCap = 2048u;
 
 // exact_kernels.cu (-fmad=false)
-void launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
-                       cudaStream_t st);
+// returns the number of kernels launched (1 fused, or K1a + K1b)
+int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f, DevCounters* ctr,
+                      cudaStream_t st);
 // K1 fused over a batch of 1 <= nv <= kMaxFusedViews views of one scene and
 // config (same bound / blend classes): each splat's inputs read once.
 constexpr int kMaxFusedViews = 4;
