@@ -131,3 +131,21 @@ def test_alpha_clamp_active(gpu, reference, kname):
     fb, ctr = gpu.render(splats, cam, cfg)
     assert ctr.as_dict() == ctr_r
     assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
+
+
+@pytest.mark.parametrize("sname", ["random", "c1"])
+@pytest.mark.parametrize("coeffs,kind", [
+    ((0.8082182210258585, -0.22859470326756573, 0.014202796808880376), api.KernelKind.PolynomialRelu),  # fitted poly2, ReLU
+    ((0.5, 0.1, -0.05), api.KernelKind.PolynomialRelu),        # rises, then falls: max inside (0, root)
+    ((0.9, -0.6, 0.09), api.KernelKind.PolynomialRelu),        # falls, then rises again past its minimum
+], ids=["poly2-relu", "rise-fall", "fall-rise"])
+def test_non_monotone_kernels(gpu, reference, sname, coeffs, kind):
+    """Kernels that are not non-increasing in q take the alpha-threshold blend
+    (the alpha < eps guard on alpha itself, every record for every pixel)."""
+    splats, deg, cam = _setup(sname)
+    k = api.make_polynomial_kernel(kind, coeffs)
+    cfg = api.RasterConfig(kernel=k, culling_mode=api.CullingMode.ZeroCrossing, sh_degree=deg)
+    rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+    fb, ctr = gpu.render(splats, cam, cfg)
+    assert ctr.as_dict() == ctr_r
+    assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
