@@ -64,7 +64,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     const uint32_t* vin = pval + r.x;                                 // bucket order (global)
     uint32_t* nk = smem;                                              // 32-bit key per bucket slot
     uint16_t* perm = reinterpret_cast<uint16_t*>(smem + CAP);          // bin-sorted position -> slot
-    uint16_t* dest = perm + CAP;                                       // bin-sorted position -> final
+    uint16_t* dest = perm + CAP;                                       // bucket slot -> final position
     uint32_t* hist = smem + S::LIST;                                  // counts -> cursors -> list
     __shared__ uint32_t red_min[WARPS], red_max[WARPS];
     __shared__ uint32_t wsum[WARPS];
@@ -142,16 +142,16 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
                 rank += before;
             }
         }
-        dest[p] = static_cast<uint16_t>(s + rank);
+        dest[j] = static_cast<uint16_t>(s + rank);
     }
     __syncthreads();
     uint32_t* list = hist;
     if (!need_bitonic) {
-        for (int p = t; p < L; p += THREADS) list[dest[p]] = vin[perm[p]];
+        for (int j = t; j < L; j += THREADS) list[dest[j]] = vin[j]; // coalesced read of the bucket
     } else {
         // degenerate depth clusters: exact bitonic sort on (bits, original index);
         // full keys over the (now dead) nk / perm / dest arrays
-        for (int p = t; p < L; p += THREADS) list[p] = vin[perm[p]];
+        for (int j = t; j < L; j += THREADS) list[j] = vin[j];
         __syncthreads();
         unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem);
         int n = 1;

@@ -15,7 +15,7 @@ def find(pat, start=0):
     raise KeyError(pat)
 
 
-k = find(r"__global__ void __launch_bounds__\(128, 6\) k_blend16")
+k = find(r"__global__ void __launch_bounds__\(128, \d\) k_blend16")
 ranges = {
     "walk": (find(r"^struct Frag \{"), find(r"^// alpha of \(pixel")),
     "stage+cover": (find(r"stage the record prefetched", k), find(r"prefetch the next batch", k)),
