@@ -882,9 +882,13 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
                       cudaStream_t st) {
     if (s.n == 0) return 0;
     const int blocks = static_cast<int>((s.n + 255) / 256);
-    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323)
+    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323),
+    // for scenes whose frame arrays stay L2-resident: measured faster at 1M
+    // splats (182 vs 203 us) but slower from 2M on (383 vs 347 us at 2M, 1.33
+    // vs 1.02 ms at 6M), where the split K1a / K1b streams HBM better
+    constexpr int64_t kFusedMaxSplats = 1500000;
 #define PS_FUSED(BCV, BKV)                                                                 \
-    if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
+    if (s.n <= kFusedMaxSplats && P.bound_class == BCV && P.blend_class == BKV) {        \
         k_preprocess<BCV, BKV><<<blocks, 256, 0, st>>>(s, P, f, ctr);                    \
         return 1;                                                                        \
     }

@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 for round in 1 2; do
   for lib in _ab/*.so; do
     echo "== $lib (round $round)"
-    PS_B200_LIB=$lib python tools/profile_frame.py --frames 30 "$@" | tail -1
+    PS_B200_LIB=$lib python tools/profile_frame.py --frames 12 "$@" | tail -1
   done
 done
 for lib in _ab/*.so; do

@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_18707_b200 import api  # noqa: E402
 
 W = {"c1": ("g", 1, 10_000, 256, 256), "c2": ("g", 2, 1_000_000, 1920, 1080),
-     "c3": ("g", 4, 6_000_000, 3840, 2160), "c5": ("skewed", 3, 1_000_000, 1920, 1080)}
+     "c3": ("g", 4, 6_000_000, 3840, 2160), "c4": ("g", 5, 3_000_000, 1920, 1080),
+     "c5": ("skewed", 3, 1_000_000, 1920, 1080), "g2m": ("g", 6, 2_000_000, 1920, 1080)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2")
