@@ -434,8 +434,11 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workl
     if dom:
         top["kernel"] = dom
         top["traffic"], top["traffic_source"] = profiled_traffic(dom, kname, workload)
-        top["peak_note"] = ("HBM peak from MEASURED_PEAKS.json" if top["bound"] == "hbm"
-                            else "FP32 issue peak measured in-run (no FP32 entry in MEASURED_PEAKS.json)")
+        if top["bound"] == "hbm":
+            top["peak_note"] = ("HBM copy bandwidth from MEASURED_PEAKS.json" if not pk.get("_fallback")
+                                else "MEASURED_PEAKS.json absent: B200_PROFILING.md fallback 6650 GB/s")
+        else:
+            top["peak_note"] = "FP32 issue peak measured in-run (no FP32 entry in MEASURED_PEAKS.json)"
     return top, out
 
 
