@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof_launches_c2_exp.csv \
     python tools/profile_frame.py --frames 3 --kernel exp --mode StopThePop > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"blend16|k_geometry|k_shade|k_preprocess|k_dup" -s 3 -c 3 \
-    -o gpurun_out/prof_full_c2 python tools/profile_frame.py --frames 2 > /dev/null 2>&1
+    -o gpurun_out/prof_full_c2 python tools/profile_frame.py --frames 3 > /dev/null 2>&1
 ncu -i gpurun_out/prof_full_c2.ncu-rep --page details --csv > gpurun_out/prof_full_c2_details.csv 2>/dev/null
 ncu -i gpurun_out/prof_full_c2.ncu-rep --page raw --csv > gpurun_out/prof_full_c2_raw.csv 2>/dev/null
 bash tools/ncu_kernel.sh blend16 prof_blend_src > /dev/null 2>&1
