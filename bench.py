@@ -294,7 +294,7 @@ def run_ours(args) -> None:
             c2 = make_cfg(api, kname, mode, deg).to_struct()
             m2, _, _, _ = timed(c2, max(3, min(args.steps, 10)), 3)
             kern[label] = {"frames_per_s": frames_per_step * 1000.0 / m2, "ms": m2 / frames_per_step,
-                           "pairs": r.stats()["pairs"]}
+                           "pairs": r.stats()["pairs"] // frames_per_step}  # per view
         # image quality of every kernel against exp / StopThePop (the paper's
         # comparison point), on the device: polysplat::compare (metrics.cpp:138-157)
         ref_cfg = make_cfg(api, "exp", "StopThePop", deg)

@@ -37,6 +37,8 @@ for r in rows:
             reg = next((n for n, (a, b) in ranges.items() if a <= ln < b), "kernel body")
         elif cur.startswith("tile_sort"):
             reg = "sort"
+        elif cur.startswith("sm_100_rt"):
+            reg = "walk"  # the packed f32x2 builtins (__ffma2_rn ...) the walk is made of
         else:
             reg = "other:" + cur
         a = agg.setdefault(reg, [0, 0])
