@@ -107,7 +107,7 @@ __device__ __forceinline__ float alpha_f32(float q, float oval, const KernelF32&
 }
 
 template <int KIND, int MODE, bool COUNT>
-__global__ void k_blend(const BlendArgs A) {
+__global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
     extern __shared__ float4 smem[];
     const int nt = blockDim.x;
     float4* s0 = smem;
@@ -790,8 +790,14 @@ void launch16_kind(const BlendArgs& a, int n_tiles, bool count, cudaStream_t st)
 
 template <int KIND, int MODE>
 void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, cudaStream_t st) {
-    if (count) k_blend<KIND, MODE, true><<<n_tiles, nt, smem, st>>>(a);
-    else k_blend<KIND, MODE, false><<<n_tiles, nt, smem, st>>>(a);
+    // tile 32: 1024 threads x 52 B of staging = 52 KB of dynamic shared memory
+    if (count) {
+        cudaFuncSetAttribute(k_blend<KIND, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_blend<KIND, MODE, true><<<n_tiles, nt, smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_blend<KIND, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_blend<KIND, MODE, false><<<n_tiles, nt, smem, st>>>(a);
+    }
 }
 
 } // namespace

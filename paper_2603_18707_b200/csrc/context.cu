@@ -595,9 +595,13 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
     // Stage the raw arrays (a few large DMAs; full link rate when the host
     // buffers are pinned), order the splats along a Morton curve of their means,
     // and gather them into the scene's SoA planes in that order.
-    const size_t geo = sizeof(double) * 11 * static_cast<size_t>(n);
-    const size_t shb = sizeof(float) * 48 * static_cast<size_t>(n);
-    const size_t sort_bytes = sizeof(uint32_t) * 4 * static_cast<size_t>(n) + radix_scratch_bytes(n) + 64;
+    // (every region 256-byte aligned: an odd n leaves 88 n bytes of fp64
+    // geometry, which would misalign the float4 SH staging after it)
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t geo = al(sizeof(double) * 11 * static_cast<size_t>(n));
+    const size_t shb = al(sizeof(float) * 48 * static_cast<size_t>(n));
+    const size_t keyb = al(sizeof(uint32_t) * 4 * static_cast<size_t>(n));
+    const size_t sort_bytes = keyb + 256 + radix_scratch_bytes(n);
     const size_t stage_bytes = geo + shb + sort_bytes + 256;
     if (stage_bytes > c->stage_bytes) {
         if (c->stage) cudaFree(c->stage);
@@ -613,8 +617,8 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
     uint32_t* keys_alt = keys + n;
     uint32_t* vals = keys + 2 * n;
     uint32_t* vals_alt = keys + 3 * n;
-    unsigned long long* bb = reinterpret_cast<unsigned long long*>(keys + 4 * n);
-    void* scratch = reinterpret_cast<char*>(bb) + 64;
+    unsigned long long* bb = reinterpret_cast<unsigned long long*>(p + geo + shb + keyb);
+    void* scratch = reinterpret_cast<char*>(bb) + 256;
     CTX_TRY(c, cudaMemcpyAsync(st, means, sizeof(double) * 3 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
