@@ -51,13 +51,9 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-// Blend kernel in fp64 for the exact decisions (set per frame, stream-ordered).
-__constant__ ps_kernel c_exact_kernel;
-__constant__ double c_exact_eps;
 
 // eval_kernel (kernel.cpp:162-172) with explicitly rounded ops (never contracted)
-__device__ double eval_kernel_rn(double x) {
-    const ps_kernel& k = c_exact_kernel;
+__device__ double eval_kernel_rn(const ps_kernel& k, double x) {
     if (k.kind == PS_KERNEL_EXPONENTIAL) return exp(dmul(-0.5, x));
     double p = k.coeffs[k.order];
     for (int i = k.order - 1; i >= 0; --i) p = dadd(dmul(p, x), k.coeffs[i]);
@@ -68,7 +64,8 @@ __device__ double eval_kernel_rn(double x) {
 // The reference's alpha decision for pixel (gx, gy) and splat i, in its exact
 // fp64 arithmetic (raster.cpp:262-271): dx = px + 0.5 - mx, q = a dx dx +
 // 2 b dx dy + c dy dy, alpha = min(0.999, o k(q)); returns !(alpha < eps).
-__device__ __noinline__ bool exact_alpha_ge_eps(const double2* __restrict__ mean2d,
+__device__ __noinline__ bool exact_alpha_ge_eps(const ps_kernel& kern, double eps,
+                                                const double2* __restrict__ mean2d,
                                                 const double2* __restrict__ conic_ab,
                                                 const double2* __restrict__ conic_cq,
                                                 const double* __restrict__ opacity_eff, uint32_t i,
@@ -81,9 +78,9 @@ __device__ __noinline__ bool exact_alpha_ge_eps(const double2* __restrict__ mean
     const double dy = dsub(dadd(static_cast<double>(gy), 0.5), m.y);
     const double q = dadd(dadd(dmul(dmul(ab.x, dx), dx), dmul(dmul(dmul(2.0, ab.y), dx), dy)),
                           dmul(dmul(cq.x, dy), dy));
-    const double v = dmul(o, eval_kernel_rn(q));
+    const double v = dmul(o, eval_kernel_rn(kern, q));
     const double alpha = (v < 0.999) ? v : 0.999;
-    return !(alpha < c_exact_eps);
+    return !(alpha < eps);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -162,7 +159,7 @@ __global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
                     if (!(q <= v1.y)) continue; // alpha < eps certainly (or pixel/splat pair skipped)
                     if (q >= v1.z) {            // inside the fp32 error band: decide in fp64
                         ++nexact;
-                        if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                        if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
                     }
                     alpha = alpha_f32<KIND>(q, v1.w, P.kf);
                 } else {
@@ -170,7 +167,7 @@ __global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
                     if (alpha < eps - v1.y) continue;
                     if (alpha < eps + v1.y) {
                         ++nexact;
-                        if (!exact_alpha_ge_eps(A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                        if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
                     }
                 }
                 const float4 v2 = s2[k];
@@ -517,7 +514,7 @@ __device__ __forceinline__ double exact_alpha(const BlendArgs& A, uint32_t i, do
     const double dy = dsub(dadd(static_cast<double>(gy), 0.5), m.y);
     const double q = dadd(dadd(dmul(dmul(ab.x, dx), dx), dmul(dmul(dmul(2.0, ab.y), dx), dy)),
                           dmul(dmul(cq.x, dy), dy));
-    const double v = dmul(o, eval_kernel_rn(q));
+    const double v = dmul(o, eval_kernel_rn(A.P.cfg.kernel, q));
     return (v < 0.999) ? v : 0.999;
 }
 
@@ -534,7 +531,7 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
     const int lx = lxy & 15, ly = lxy >> 4;
     const int gx = px0 + lx, gy = py0 + ly;
     const float xc = lx + 0.5f, yc = ly + 0.5f;
-    const double eps = c_exact_eps, floor_t = A.P.cfg.transmittance_floor;
+    const double eps = A.P.cfg.epsilon, floor_t = A.P.cfg.transmittance_floor;
     double trans = 1.0, r = 0.0, g = 0.0, b = 0.0;
     unsigned long long evals = 0, blended = 0;
     bool done = false;
@@ -833,8 +830,6 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     const size_t smem = static_cast<size_t>(nt) * (3 * sizeof(float4) + sizeof(uint32_t));
     const int n_tiles = P.tiles_x * P.tiles_y;
     if (n_tiles == 0) return 0;
-    cudaMemcpyToSymbolAsync(c_exact_kernel, &P.cfg.kernel, sizeof(ps_kernel), 0, cudaMemcpyHostToDevice, st);
-    cudaMemcpyToSymbolAsync(c_exact_eps, &P.cfg.epsilon, sizeof(double), 0, cudaMemcpyHostToDevice, st);
     if (ts == 16) {
         if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, st);
         else launch16_kind<kAlphaThreshold>(a, n_tiles, count_work, st);

@@ -89,6 +89,9 @@ struct ps_ctx {
 
 namespace {
 
+// bytes of a context's device counters block (padded; the per-tile counts follow)
+constexpr size_t kCtrBytes = (sizeof(DevCounters) + 255) & ~size_t(255);
+
 int set_err(ps_ctx* c, int code, const std::string& msg) {
     if (c) c->err = msg;
     g_free_error = msg;
@@ -218,15 +221,19 @@ int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
     }
     if (n_tiles > c->tiles_cap) {
         if (c->f.ranges) cudaFree(c->f.ranges);
-        if (c->f.tile_count) cudaFree(c->f.tile_count);
         if (c->f.big_tiles) cudaFree(c->f.big_tiles);
         c->f.ranges = nullptr;
-        c->f.tile_count = nullptr;
         c->f.big_tiles = nullptr;
         c->tiles_cap = 0;
         CTX_TRY(c, cudaMalloc(&c->f.ranges, sizeof(uint2) * n_tiles));
-        CTX_TRY(c, cudaMalloc(&c->f.tile_count, sizeof(uint32_t) * n_tiles));
         CTX_TRY(c, cudaMalloc(&c->f.big_tiles, sizeof(uint32_t) * n_tiles));
+        // the device counters and the per-tile counts share one block, so one
+        // memset clears both at the start of a frame (frame_zero_bytes)
+        void* blk = nullptr;
+        CTX_TRY(c, cudaMalloc(&blk, kCtrBytes + sizeof(uint32_t) * n_tiles));
+        cudaFree(c->d_ctr);
+        c->d_ctr = static_cast<DevCounters*>(blk);
+        c->f.tile_count = reinterpret_cast<uint32_t*>(static_cast<char*>(blk) + kCtrBytes);
         c->tiles_cap = n_tiles;
     }
     return PS_OK;
@@ -412,8 +419,8 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     if (req.mode == Mode::Prepare) f.tile_count = nullptr;
     record(c, 0);
     if (!req.k1_done) {
-        CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, sizeof(DevCounters), strm));
-        if (f.tile_count) CTX_TRY(c, cudaMemsetAsync(f.tile_count, 0, sizeof(uint32_t) * n_tiles, strm));
+        // counters (+ the per-tile counts right after them) in one memset
+        CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, kCtrBytes + (f.tile_count ? sizeof(uint32_t) * n_tiles : 0), strm));
         // K1: preprocess (+ tight pair count per tile)
         launches += launch_preprocess(s->dev, P, f, c->d_ctr, strm);
     }
@@ -705,7 +712,7 @@ int ps_ctx_create(int device, ps_ctx** out) {
     if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "stream");
     for (auto& ev : c->ev)
         if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(e, "event");
-    if ((e = cudaMalloc(&c->d_ctr, sizeof(DevCounters))) != cudaSuccess) return fail(e, "counters");
+    if ((e = cudaMalloc(&c->d_ctr, kCtrBytes)) != cudaSuccess) return fail(e, "counters");
     if ((e = cudaMallocHost(&c->h_ctr, sizeof(DevCounters))) != cudaSuccess) return fail(e, "pinned counters");
     *out = c;
     return PS_OK;
@@ -721,7 +728,7 @@ void ps_ctx_destroy(ps_ctx* c) {
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
     void* bufs[] = {c->n_block, c->p_block, c->radix_scratch, c->scan_scratch, c->img_rgb, c->img_t,
-                    c->f.flags, c->f.ranges, c->f.tile_count, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage,
+                    c->f.flags, c->f.ranges, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage,
                     c->metrics_acc, c->cmp_block};
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -860,8 +867,7 @@ int issue_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, const ps_co
         f[k].cov_aa = nullptr;
         f[k].replay_vals = nullptr;
         ctr[k] = v->d_ctr;
-        CTX_TRY(c, cudaMemsetAsync(v->d_ctr, 0, sizeof(DevCounters), c->stream));
-        CTX_TRY(c, cudaMemsetAsync(v->f.tile_count, 0, sizeof(uint32_t) * n_tiles, c->stream));
+        CTX_TRY(c, cudaMemsetAsync(v->d_ctr, 0, kCtrBytes + sizeof(uint32_t) * n_tiles, c->stream));
     }
     if (c->timing) cudaEventRecord(c->ev[0], c->stream);
     launch_preprocess_views(s->dev, P, f, ctr, vb.nv, c->stream);

@@ -11,15 +11,15 @@ import torch  # noqa: E402
 from paper_2603_18707_b200 import api  # noqa: E402
 
 lib = api.lib()
-for kind, n in (("g", 1000), ("g", 1_000_000)):
+for kind, n, w, h in (("g", 1000, 64, 64), ("g", 1_000_000, 1920, 1080)):
     sc = api.Scene.synthetic(kind, 2, n)
     r = api.Rasterizer(0)
     ds = r.upload(sc)
-    cam = api.orbit_cameras(256, 1920, 1080)[0].to_struct()
+    cam = api.orbit_cameras(256, w, h)[0].to_struct()
     cfg = api.RasterConfig(kernel=api.fitted_kernel("poly1"), culling_mode=api.CullingMode.OpacityAware,
                            sh_degree=3).to_struct()
-    rgb = torch.empty((1080, 1920, 3), device="cuda")
-    t = torch.empty((1080, 1920), device="cuda")
+    rgb = torch.empty((h, w, 3), device="cuda")
+    t = torch.empty((h, w), device="cuda")
     stream = torch.cuda.ExternalStream(lib.ps_ctx_stream(r.handle))
 
     def one():
