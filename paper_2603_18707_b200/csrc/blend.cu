@@ -602,12 +602,12 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 }
 
 template <int KIND, int ORDER, int MODE, bool COUNT>
-__global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
+__global__ void __launch_bounds__(128, 9) k_blend16(const BlendArgs A) {
     using SortSm = TileSortSmem<128, kBlendSortCap / 128>;
     static_assert(SortSm::CAP == static_cast<int>(kBlendSortCap), "prologue sort capacity");
     // Shared memory: the bucket sort's workspace; the sorted list starts at word
     // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
-    // overlay the sort's dead arrays below it. 8 CTAs (32 warps) per SM.
+    // overlay the sort's dead arrays below it. 9 CTAs (36 warps) per SM.
     __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];
@@ -647,7 +647,8 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     // one CTA, presorted in global memory otherwise
     const uint32_t* list = A.pval + range.x;
     if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, kBlendSortCap / 128, false>(range, A.pval_w, A.pkey, A.key, A.orig, S);
+        list = sort_one_tile<128, kBlendSortCap / 128, false>(range, A.pval_w, A.pkey, A.key, A.orig, S,
+                                                              &A.ctr->unsorted);
         __syncthreads();
     }
     double2 pm = make_double2(0.0, 0.0);

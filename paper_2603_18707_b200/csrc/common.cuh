@@ -57,7 +57,7 @@ struct DevCounters {
     unsigned long long key_min;      // complement of the min / max fp64 depth bits (visible splats)
     unsigned long long key_max;
     unsigned int big_tiles;          // tiles with > 1024 pairs (listed in FrameDev::big_tiles)
-    unsigned int pad2;
+    unsigned int unsorted;           // a blend-prologue bucket sort could not run (re-run presorted)
 };
 
 // Per-splat frame arrays (indexed by original splat index).

@@ -256,6 +256,7 @@ struct FrameRequest {
     bool no_speculation = false; // force the synchronous (sized) path
     bool k1_done = false;        // K1 (and the counter / tile-count zeroing) already issued by a view batch
     bool defer = false;          // speculative path: return kPending instead of the end-of-frame sync
+    bool presort_all = false;    // every bucket sorted by the list kernels before the blend
 };
 
 // run_frame status: the speculative frame is queued, finish_frame() completes it
@@ -375,11 +376,12 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
     const bool long_sorts = c->last_max_len > kBlendSortCap;
     c->last_max_len = res.ctr.max_tile_len;
     if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
-        (!long_sorts && res.ctr.max_tile_len > kBlendSortCap)) {
+        (!long_sorts && res.ctr.max_tile_len > kBlendSortCap) || res.ctr.unsorted) {
         FrameRequest sized = req;
         sized.no_speculation = true;
         sized.k1_done = false;
         sized.defer = false;
+        sized.presort_all = res.ctr.unsorted != 0; // a prologue sort could not run
         return run_frame(c, s, cam, cfg_in, sized, res);
     }
     frame_stats(c, res);
@@ -442,6 +444,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     }
     record(c, 2);
     if (req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 && !req.no_speculation &&
+        !req.presort_all &&
         c->last_max_len <= kMaxBucketSorted) {
         // Speculative frame: no host round trip between the count scan and the
         // blend. The pair buffers from earlier frames are used as they are;
@@ -496,7 +499,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         // K4: exact (depth, index) order inside every bucket — long buckets
         // here, buckets of <= 1024 in the blend prologue (16x16 tiles), all of
         // them here for the tile-list query or other tile sizes
-        if (req.mode == Mode::Render && cfg.tile_size == 16) {
+        if (req.mode == Mode::Render && cfg.tile_size == 16 && !req.presort_all) {
             launch_tile_sort_long(f, s->dev.orig, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
             sort_in_blend = f.pval;
         } else {
@@ -549,6 +552,14 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     CTX_TRY(c, cudaGetLastError());
     res.ctr = *c->h_ctr;
     c->last_max_len = res.ctr.max_tile_len;
+    if (res.ctr.unsorted && !req.presort_all) { // a prologue sort could not run: every bucket presorted
+        FrameRequest again = req;
+        again.no_speculation = true;
+        again.k1_done = false;
+        again.defer = false;
+        again.presort_all = true;
+        return run_frame(c, s, cam, cfg_in, again, res);
+    }
     res.launches = launches;
     frame_stats(c, res);
     return PS_OK;

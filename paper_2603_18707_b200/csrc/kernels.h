@@ -13,7 +13,7 @@ namespace ps {
 constexpr uint32_t kMaxBucketSorted = 12288u;
 // Longest bucket the blend kernel sorts in its prologue (16x16 tiles); longer
 // ones are sorted by the list kernels (binning.cu) before the blend.
-constexpr uint32_t kBlendSortCap = 2048u;
+constexpr uint32_t kBlendSortCap = 1536u; // 18 KB of shared memory: 9 CTAs per SM
 
 // exact_kernels.cu (-fmad=false)
 // returns the number of kernels launched (1 fused, or K1a + K1b)

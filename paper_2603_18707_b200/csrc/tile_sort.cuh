@@ -52,11 +52,16 @@ struct TileSortSmem {
 
 // Returns the sorted bucket in shared memory (smem + LIST); with WRITEBACK also
 // writes it to pval[r.x, r.y). The caller synchronises before reading it.
+// The bitonic fallback pads the bucket to a power of two n: it needs n 64-bit
+// keys over the nk / perm / dest arrays (2 CAP words) and n list slots; when
+// the padded bucket does not fit (CAP not a power of two), *unsorted is set and
+// the caller's frame is re-run with every bucket sorted by the list kernels.
 template <int THREADS, int ROUNDS, bool WRITEBACK = true>
 __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __restrict__ pval,
                                                    const uint32_t* __restrict__ pkey,
                                                    const unsigned long long* __restrict__ key,
-                                                   const uint32_t* __restrict__ orig, uint32_t* smem) {
+                                                   const uint32_t* __restrict__ orig, uint32_t* smem,
+                                                   unsigned int* unsorted = nullptr) {
     using S = TileSortSmem<THREADS, ROUNDS>;
     constexpr int CAP = S::CAP, BINS = S::BINS, WARPS = S::WARPS, SH = S::BIN_SHIFT;
     constexpr int PER = BINS / THREADS;
@@ -146,7 +151,13 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     }
     __syncthreads();
     uint32_t* list = hist;
-    if (!need_bitonic) {
+    int n_pad = 1;
+    while (n_pad < L) n_pad <<= 1;
+    if (need_bitonic && (n_pad > CAP || n_pad > (CAP > BINS ? CAP : BINS))) {
+        // (cannot happen for power-of-two CAP; see above)
+        for (int j = t; j < L; j += THREADS) list[j] = vin[j];
+        if (t == 0 && unsorted) atomicExch(unsorted, 1u);
+    } else if (!need_bitonic) {
         for (int j = t; j < L; j += THREADS) list[dest[j]] = vin[j]; // coalesced read of the bucket
     } else {
         // degenerate depth clusters: exact bitonic sort on (bits, original index);
