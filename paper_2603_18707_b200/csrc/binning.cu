@@ -21,11 +21,12 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanPer = 16; // consecutive tiles per thread per round (16K tiles per round)
 
 // One CTA: exclusive scan of the per-tile pair counts into ranges and K3
-// cursors, the total / longest bucket, and the list of buckets > kBlendSortCap (sorted
+// cursors, the total / longest bucket, and the list of buckets > list_min (sorted
 // outside the blend). Each thread owns 16 consecutive tiles (vector loads and
 // stores), so a 1080p frame (8160 tiles) is one round.
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict__ count, uint2* __restrict__ ranges,
-                                                            int n_tiles, DevCounters* ctr, uint32_t* __restrict__ big_list) {
+                                                            int n_tiles, DevCounters* ctr, uint32_t* __restrict__ big_list,
+                                                            uint32_t list_min) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t wmax[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
 #pragma unroll
             for (int q = 0; q < kScanPer; ++q) {
                 cur[q] = excl;
-                if (v[q] > kBlendSortCap) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
+                if (v[q] > list_min) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
                 excl += v[q];
             }
 #pragma unroll
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
                 if (t < n_tiles) {
                     ranges[t] = make_uint2(excl, excl + v[q]);
                     count[t] = excl;
-                    if (v[q] > kBlendSortCap) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
+                    if (v[q] > list_min) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
                 }
                 excl += v[q];
             }
@@ -145,8 +146,8 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
 } // namespace
 
 void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
-                      cudaStream_t st) {
-    k_tile_scan<<<1, kScanThreads, 0, st>>>(tile_count, ranges, n_tiles, ctr, big_list);
+                      uint32_t list_min, cudaStream_t st) {
+    k_tile_scan<<<1, kScanThreads, 0, st>>>(tile_count, ranges, n_tiles, ctr, big_list, list_min);
 }
 
 // Bucket length <= 1024: 128 threads per tile over all tiles; longer buckets
@@ -160,11 +161,11 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
     k_tile_sort_small<128, 16><<<n_tiles, 128, S1::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.gate,
                                                                   f.pair_cap);
     if (launches) *launches += 1;
-    if (max_len > kBlendSortCap) {
+    if (max_len > 2048u) {
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
         k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, kBlendSortCap, f.gate, f.pair_cap);
+                                                                   &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
@@ -179,15 +180,16 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
 
 // max_len == 0xffffffff: unknown on the host (speculative frame) -- launch both
 // list kernels; they read the device-built list and exit when it is empty.
-bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
-                           cudaStream_t st, int* launches) {
+bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, uint32_t cap,
+                           const DevCounters* d_ctr, cudaStream_t st, int* launches) {
     const bool unknown = max_len == 0xffffffffu;
-    if (max_len <= kBlendSortCap) return true;
+    if (max_len <= cap) return true;
     if (max_len > kMaxBucketSorted && !unknown) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
     k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
-                                                               &d_ctr->big_tiles, kBlendSortCap, f.gate, f.pair_cap);
+                                                               &d_ctr->big_tiles, static_cast<int>(cap), f.gate,
+                                                               f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;

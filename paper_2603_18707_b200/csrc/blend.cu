@@ -601,10 +601,11 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
     }
 }
 
-template <int KIND, int ORDER, int MODE, bool COUNT>
-__global__ void __launch_bounds__(128, 9) k_blend16(const BlendArgs A) {
-    using SortSm = TileSortSmem<128, kBlendSortCap / 128>;
-    static_assert(SortSm::CAP == static_cast<int>(kBlendSortCap), "prologue sort capacity");
+// CAPR: rounds of the prologue sort (12: buckets <= 1536 in 18 KB of shared
+// memory, 9 CTAs per SM; 16: <= 2048 in 24 KB, 8 CTAs per SM)
+template <int KIND, int ORDER, int MODE, bool COUNT, int CAPR>
+__global__ void __launch_bounds__(128, CAPR <= 12 ? 9 : 8) k_blend16(const BlendArgs A) {
+    using SortSm = TileSortSmem<128, CAPR>;
     // Shared memory: the bucket sort's workspace; the sorted list starts at word
     // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
     // overlay the sort's dead arrays below it. 9 CTAs (36 warps) per SM.
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(128, 9) k_blend16(const BlendArgs A) {
     // one CTA, presorted in global memory otherwise
     const uint32_t* list = A.pval + range.x;
     if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, kBlendSortCap / 128, false>(range, A.pval_w, A.pkey, A.key, A.orig, S,
+        list = sort_one_tile<128, CAPR, false>(range, A.pval_w, A.pkey, A.key, A.orig, S,
                                                               &A.ctr->unsorted);
         __syncthreads();
     }
@@ -772,18 +773,23 @@ __global__ void __launch_bounds__(128, 9) k_blend16(const BlendArgs A) {
 }
 
 template <int KIND, int ORDER, int MODE>
-void launch16(const BlendArgs& a, int n_tiles, bool count, cudaStream_t st) {
-    if (count) k_blend16<KIND, ORDER, MODE, true><<<n_tiles, 128, 0, st>>>(a);
-    else k_blend16<KIND, ORDER, MODE, false><<<n_tiles, 128, 0, st>>>(a);
+void launch16(const BlendArgs& a, int n_tiles, bool count, uint32_t cap, cudaStream_t st) {
+    if (cap <= kBlendSortCapSmall) {
+        if (count) k_blend16<KIND, ORDER, MODE, true, kBlendSortCapSmall / 128><<<n_tiles, 128, 0, st>>>(a);
+        else k_blend16<KIND, ORDER, MODE, false, kBlendSortCapSmall / 128><<<n_tiles, 128, 0, st>>>(a);
+    } else {
+        if (count) k_blend16<KIND, ORDER, MODE, true, kBlendSortCapLarge / 128><<<n_tiles, 128, 0, st>>>(a);
+        else k_blend16<KIND, ORDER, MODE, false, kBlendSortCapLarge / 128><<<n_tiles, 128, 0, st>>>(a);
+    }
 }
 
 template <int MODE>
-void launch16_kind(const BlendArgs& a, int n_tiles, bool count, cudaStream_t st) {
+void launch16_kind(const BlendArgs& a, int n_tiles, bool count, uint32_t cap, cudaStream_t st) {
     const KernelF32& kf = a.P.kf;
-    if (kf.kind == PS_KERNEL_EXPONENTIAL) launch16<0, 1, MODE>(a, n_tiles, count, st);
-    else if (kf.order == 1) launch16<1, 1, MODE>(a, n_tiles, count, st);
-    else if (kf.order == 2) launch16<1, 2, MODE>(a, n_tiles, count, st);
-    else launch16<1, 3, MODE>(a, n_tiles, count, st);
+    if (kf.kind == PS_KERNEL_EXPONENTIAL) launch16<0, 1, MODE>(a, n_tiles, count, cap, st);
+    else if (kf.order == 1) launch16<1, 1, MODE>(a, n_tiles, count, cap, st);
+    else if (kf.order == 2) launch16<1, 2, MODE>(a, n_tiles, count, cap, st);
+    else launch16<1, 3, MODE>(a, n_tiles, count, cap, st);
 }
 
 template <int KIND, int MODE>
@@ -801,8 +807,8 @@ void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, 
 } // namespace
 
 int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
-                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st,
-                 bool* replay_fused) {
+                 uint32_t sort_cap, const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work,
+                 cudaStream_t st, bool* replay_fused) {
     *replay_fused = false;
     BlendArgs a;
     a.P = P;
@@ -832,8 +838,8 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     const int n_tiles = P.tiles_x * P.tiles_y;
     if (n_tiles == 0) return 0;
     if (ts == 16) {
-        if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, st);
-        else launch16_kind<kAlphaThreshold>(a, n_tiles, count_work, st);
+        if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, sort_cap, st);
+        else launch16_kind<kAlphaThreshold>(a, n_tiles, count_work, sort_cap, st);
         *replay_fused = true; // flagged pixels are replayed inside k_blend16
         return 1;
     }

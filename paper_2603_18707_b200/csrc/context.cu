@@ -373,10 +373,11 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
     CTX_TRY(c, cudaGetLastError());
     int st = check_frame_counters(c, s, res);
     if (st != PS_OK) return st;
-    const bool long_sorts = c->last_max_len > kBlendSortCap;
+    const uint32_t cap = blend_sort_cap(c->last_max_len); // what the speculative frame ran with
+    const bool long_sorts = c->last_max_len > cap;
     c->last_max_len = res.ctr.max_tile_len;
     if (res.pairs > c->p_cap || res.ctr.max_tile_len > kMaxBucketSorted ||
-        (!long_sorts && res.ctr.max_tile_len > kBlendSortCap) || res.ctr.unsorted) {
+        (!long_sorts && res.ctr.max_tile_len > cap) || res.ctr.unsorted) {
         FrameRequest sized = req;
         sized.no_speculation = true;
         sized.k1_done = false;
@@ -427,6 +428,9 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         launches += launch_preprocess(s->dev, P, f, c->d_ctr, strm);
     }
     record(c, 1);
+    // speculative frame: no host round trip between the count scan and the blend (below)
+    const bool speculative = req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 &&
+                             !req.no_speculation && !req.presort_all && c->last_max_len <= kMaxBucketSorted;
     const uint32_t* order = nullptr;
     if (req.mode == Mode::Prepare) {
         // prepare_splats needs the global (depth, index) order: stable radix
@@ -439,13 +443,15 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
                              &launches);
     } else {
         // K2: tile ranges + bucket cursors from the per-tile counts (K1a)
-        launch_tile_scan(f.tile_count, f.ranges, n_tiles, c->d_ctr, f.big_tiles, strm);
+        // a speculative frame lists the buckets its prologue cannot sort; a sized
+        // frame lists every bucket above the smaller capacity (its cap is chosen
+        // after this scan)
+        launch_tile_scan(f.tile_count, f.ranges, n_tiles, c->d_ctr, f.big_tiles,
+                         speculative ? blend_sort_cap(c->last_max_len) : kBlendSortCapSmall, strm);
         launches += 1;
     }
     record(c, 2);
-    if (req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 && !req.no_speculation &&
-        !req.presort_all &&
-        c->last_max_len <= kMaxBucketSorted) {
+    if (speculative) {
         // Speculative frame: no host round trip between the count scan and the
         // blend. The pair buffers from earlier frames are used as they are;
         // K3 / the long-bucket sorts / the blend do nothing when this frame's
@@ -461,12 +467,13 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         record(c, 4);
         // buckets > kBlendSortCap (sorted outside the blend): launched when the
         // last frame had any; a frame that has them unannounced is re-run
-        const bool long_sorts = c->last_max_len > kBlendSortCap;
-        if (long_sorts) launch_tile_sort_long(f, s->dev.orig, 0xffffffffu, c->d_ctr, strm, &launches);
+        const uint32_t cap = blend_sort_cap(c->last_max_len);
+        const bool long_sorts = c->last_max_len > cap;
+        if (long_sorts) launch_tile_sort_long(f, s->dev.orig, 0xffffffffu, cap, c->d_ctr, strm, &launches);
         record(c, 5);
         BlendOut out{req.d_rgb, req.d_t};
         bool replay_fused = false;
-        launches += launch_blend(f, P, f.pval, f.pval, s->dev.orig, c->d_ctr, out, req.count_work, strm,
+        launches += launch_blend(f, P, f.pval, f.pval, cap, s->dev.orig, c->d_ctr, out, req.count_work, strm,
                                  &replay_fused);
         record(c, 6);
         record(c, 7);
@@ -491,6 +498,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
     const uint32_t* svals = f.pval;
     uint32_t* sort_in_blend = nullptr;
+    uint32_t sort_cap = kBlendSortCapLarge;
     if (res.ctr.max_tile_len <= kMaxBucketSorted) {
         // K3: scatter splat indices into per-tile buckets
         launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
@@ -500,7 +508,8 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         // here, buckets of <= 1024 in the blend prologue (16x16 tiles), all of
         // them here for the tile-list query or other tile sizes
         if (req.mode == Mode::Render && cfg.tile_size == 16 && !req.presort_all) {
-            launch_tile_sort_long(f, s->dev.orig, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
+            sort_cap = blend_sort_cap(res.ctr.max_tile_len);
+            launch_tile_sort_long(f, s->dev.orig, res.ctr.max_tile_len, sort_cap, c->d_ctr, strm, &launches);
             sort_in_blend = f.pval;
         } else {
             launch_tile_sort(f, s->dev.orig, n_tiles, res.ctr.max_tile_len, c->d_ctr, strm, &launches);
@@ -536,8 +545,8 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     // K6: blend
     BlendOut out{req.d_rgb, req.d_t};
     bool replay_fused = false;
-    launches += launch_blend(f, P, svals, sort_in_blend, s->dev.orig, c->d_ctr, out, req.count_work, strm,
-                             &replay_fused);
+    launches += launch_blend(f, P, svals, sort_in_blend, sort_cap, s->dev.orig, c->d_ctr, out, req.count_work,
+                             strm, &replay_fused);
     record(c, 6);
     if (!replay_fused) {
         // K7: exact replay of flagged pixels (grid-stride over the device-side count)

@@ -11,9 +11,16 @@ namespace ps {
 // Longest per-tile bucket sorted in shared memory (binning.cu); longer tiles
 // take the global radix-sort path.
 constexpr uint32_t kMaxBucketSorted = 12288u;
-// Longest bucket the blend kernel sorts in its prologue (16x16 tiles); longer
-// ones are sorted by the list kernels (binning.cu) before the blend.
-constexpr uint32_t kBlendSortCap = 1536u; // 18 KB of shared memory: 9 CTAs per SM
+// Longest bucket the blend kernel sorts in its prologue (16x16 tiles), chosen
+// per frame from the previous frame's longest bucket: 1536 (18 KB of shared
+// memory, 9 CTAs per SM) or 2048 (24 KB, 8 CTAs per SM); longer buckets are
+// sorted by the list kernels (binning.cu) before the blend. K2 lists every
+// bucket longer than the smaller capacity.
+constexpr uint32_t kBlendSortCapSmall = 1536u;
+constexpr uint32_t kBlendSortCapLarge = 2048u;
+inline uint32_t blend_sort_cap(uint32_t longest_bucket) {
+    return longest_bucket <= kBlendSortCapSmall ? kBlendSortCapSmall : kBlendSortCapLarge;
+}
 
 // exact_kernels.cu (-fmad=false)
 // returns the number of kernels launched (1 fused, or K1a + K1b)
@@ -58,8 +65,9 @@ void launch_ranges(const uint32_t* keys, const uint32_t* d_n, int64_t n_cap, uin
                    int n_tiles, cudaStream_t st, int* launches);
 
 // binning.cu — per-tile buckets (K2 tile scan, K4 per-tile exact depth sort)
+// list_min: buckets longer than this go to the long-bucket list (sorted before the blend)
 void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
-                      cudaStream_t st);
+                      uint32_t list_min, cudaStream_t st);
 // sorts every bucket with 1 < length <= max_items (shared memory); returns false
 // when max_items exceeds what one CTA can hold (caller falls back)
 bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint32_t max_len,
@@ -73,11 +81,11 @@ struct BlendOut {
 // sort_in_place: buckets of <= 1024 entries still unsorted (sorted in the blend
 // prologue and written back); null when every bucket is already sorted.
 int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
-                 const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work, cudaStream_t st,
-                 bool* replay_fused);
+                 uint32_t sort_cap, const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work,
+                 cudaStream_t st, bool* replay_fused);
 // sort only buckets longer than min_len (the blend prologue handles the rest)
-bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, const DevCounters* d_ctr,
-                           cudaStream_t st, int* launches);
+bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, uint32_t cap,
+                           const DevCounters* d_ctr, cudaStream_t st, int* launches);
 
 // metrics.cu — composite + PSNR / max-abs / SSIM of two framebuffers
 // (fp32 or fp64, device pointers) against background bg; synchronises st.
