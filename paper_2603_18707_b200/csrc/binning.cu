@@ -164,7 +164,7 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
     if (max_len > 2048u) {
         using S2 = TileSortSmem<512, 8>;
         cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-        k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
+        k_tile_sort_list<512, 8><<<148 * 4, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 2048, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
@@ -187,7 +187,7 @@ bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max
     if (max_len > kMaxBucketSorted && !unknown) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-    k_tile_sort_list<512, 8><<<148 * 2, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
+    k_tile_sort_list<512, 8><<<148 * 4, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
                                                                &d_ctr->big_tiles, static_cast<int>(cap), f.gate,
                                                                f.pair_cap);
     if (launches) *launches += 1;
