@@ -15,14 +15,14 @@ def find(pat, start=0):
     raise KeyError(pat)
 
 
-k = find(r"__global__ void __launch_bounds__\(128, \d\) k_blend16")
+k = find(r"__global__ void __launch_bounds__\(128, .*\) k_blend16")
 ranges = {
     "walk": (find(r"^struct Frag \{"), find(r"^// alpha of \(pixel")),
     "stage+cover": (find(r"stage the record prefetched", k), find(r"prefetch the next batch", k)),
     "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Shared-memory record")),
     "transpose": (find(r"warp_transpose32\(uint32_t x"), find(r"^// ---- packed fp32 pairs")),
     "group loop": (find(r"for \(int g = 0; g < kB16 / 32", k), find(r"unsigned long long ev = 0, bl = 0;", k)),
-    "replay": (find(r"^// alpha of \(pixel"), find(r"^template <int KIND, int ORDER, int MODE, bool COUNT>", k - 3)),
+    "replay": (find(r"^// alpha of \(pixel"), find(r"^template <int KIND, int ORDER, int MODE, bool COUNT", k - 6)),
 }
 hdr = next(r for r in rows if r and r[0] == "Line No")
 si, ii = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
