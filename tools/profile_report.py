@@ -40,6 +40,12 @@ def raw_metrics(path):
         "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy",
         "sm__inst_executed.avg.per_cycle_active": "ipc",
         "launch__registers_per_thread": "regs",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu",
     }
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
     out = []
@@ -85,6 +91,13 @@ def main():
             print(f"| `{d['name']}` | {t:.1f} | {d.get('dram_rd', 0):.1f} | {d.get('dram_wr', 0):.1f} | "
                   f"{mb / t * 1e3 if t else 0:.0f} | {d.get('inst', 0) / 1e6:.1f} | "
                   f"{d.get('regs', 0):.0f} | {d.get('occupancy', 0):.1f} |")
+        print()
+        print("Pipe utilisation (% of peak, active cycles) — the north star's FP32-FMA evidence for the blend:\n")
+        print("| kernel | issue slots | FMA pipe (FFMA/FFMA2/FMUL) | ALU | FP64 | XU (MUFU, conversions) | LSU |")
+        print("|---|---:|---:|---:|---:|---:|---:|")
+        for d in raw_metrics(a.raw):
+            print(f"| `{d['name']}` | {d.get('issue', 0):.1f} | {d.get('fma', 0):.1f} | {d.get('alu', 0):.1f} | "
+                  f"{d.get('fp64', 0):.1f} | {d.get('xu', 0):.1f} | {d.get('lsu', 0):.1f} |")
         print()
 
 
