@@ -505,10 +505,19 @@ def cpu_baseline(workload: str, ours=None) -> dict:
             ref.render(splats, cam, cfg)
             ts.append(time.perf_counter() - t0)
         ms = 1000.0 * statistics.median(ts)
+        # the reference's stage split: count_pairs = prepare_splats +
+        # bin_splats (raster.cpp:310-318); the rest of render is the blend
+        tc = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref.count_pairs(splats, cam, cfg)
+            tc.append(time.perf_counter() - t0)
+        mc = 1000.0 * statistics.median(tc)
         parity = full_size_parity(ours, ref_out) if ours is not None else None
         return {"parity": parity, "value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0), "kind": "reference",
-                "ms_per_frame": ms, "sample": f"median of 3 full {workload.upper()} frames ({HEADLINE[0]}), "
-                                               "polysplat::render built from the reference sources, all host threads"}
+                "ms_per_frame": ms, "stage_split_ms": {"prepare_and_bin": mc, "blend": ms - mc},
+                "sample": f"median of 3 full {workload.upper()} frames ({HEADLINE[0]}), "
+                          "polysplat::render built from the reference sources, all host threads"}
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": "frames/s", "cores": None, "kind": "reference", "sample": f"unavailable: {e}"}
 
