@@ -1,0 +1,10 @@
+#!/bin/bash
+# compute-sanitizer over tools/sanitize_run.py: memcheck, racecheck
+# (shared-memory hazards), synccheck (barrier misuse), initcheck (uninitialised
+# device reads). Summaries into gpurun_out/sanitize_*.txt.
+cd "$(dirname "$0")/.."
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py \
+      > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "$tool: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_$tool.txt | tail -1)"
+done
