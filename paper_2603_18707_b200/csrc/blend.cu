@@ -26,6 +26,7 @@ namespace {
 struct BlendArgs {
     FrameParams P;
     const uint2* ranges;
+    const uint32_t* order;             // CTA -> tile (longest bucket first; null: row-major)
     const uint32_t* pval;
     uint32_t* pval_w;                  // buckets to sort in the prologue (null: presorted)
     const uint32_t* pkey;              // coarse depth key per bucket entry (K3)
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
     uint32_t* si = reinterpret_cast<uint32_t*>(s2 + nt);
 
     const FrameParams& P = A.P;
-    const int tile = blockIdx.x;
+    const int tile = A.order ? static_cast<int>(A.order[blockIdx.x]) : static_cast<int>(blockIdx.x);
     const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
     const int ts = P.cfg.tile_size;
     const int W = P.cam.width, H = P.cam.height;
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(128, CAPR <= 12 ? 9 : 8) k_blend16(const Blend
 
     if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
     const FrameParams& P = A.P;
-    const int tile = blockIdx.x;
+    const int tile = A.order ? static_cast<int>(A.order[blockIdx.x]) : static_cast<int>(blockIdx.x);
     const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
     const int W = P.cam.width, H = P.cam.height;
     const int px0 = tx * 16, py0 = ty * 16;
@@ -813,6 +814,7 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     BlendArgs a;
     a.P = P;
     a.ranges = f.ranges;
+    a.order = f.tile_order;
     a.pval = pair_vals;
     a.pval_w = sort_in_place;
     a.pkey = f.pkey;

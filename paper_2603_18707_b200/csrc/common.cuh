@@ -85,6 +85,7 @@ struct FrameDev {
     uint32_t* pval_alt = nullptr;
     uint2* ranges = nullptr;            // per tile [start, end)
     uint32_t* big_tiles = nullptr;      // ids of tiles with > 1024 pairs
+    uint32_t* tile_order = nullptr;     // tile ids, longest bucket first (K2; the blend's CTA -> tile map)
     uint32_t* tile_count = nullptr;     // pairs per tile (K1a), then the K3 bucket cursors
     uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
     double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)

@@ -222,11 +222,14 @@ int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
     if (n_tiles > c->tiles_cap) {
         if (c->f.ranges) cudaFree(c->f.ranges);
         if (c->f.big_tiles) cudaFree(c->f.big_tiles);
+        if (c->f.tile_order) cudaFree(c->f.tile_order);
         c->f.ranges = nullptr;
         c->f.big_tiles = nullptr;
+        c->f.tile_order = nullptr;
         c->tiles_cap = 0;
         CTX_TRY(c, cudaMalloc(&c->f.ranges, sizeof(uint2) * n_tiles));
         CTX_TRY(c, cudaMalloc(&c->f.big_tiles, sizeof(uint32_t) * n_tiles));
+        CTX_TRY(c, cudaMalloc(&c->f.tile_order, sizeof(uint32_t) * n_tiles));
         // the device counters and the per-tile counts share one block, so one
         // memset clears both at the start of a frame (frame_zero_bytes)
         void* blk = nullptr;
@@ -432,6 +435,9 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     const bool speculative = req.mode == Mode::Render && cfg.tile_size == 16 && c->p_cap > 0 &&
                              !req.no_speculation && !req.presort_all && c->last_max_len <= kMaxBucketSorted;
     const uint32_t* order = nullptr;
+    // heavy-first tile order for the blend, built by an extra CTA of K3 (render
+    // frames through the bucketed path only; row-major otherwise)
+    if (req.mode != Mode::Render || n_tiles > kTileOrderMax) f.tile_order = nullptr;
     if (req.mode == Mode::Prepare) {
         // prepare_splats needs the global (depth, index) order: stable radix
         // sort of the fp64 depth bits (culled splats carry ~0 and sort last)
@@ -462,8 +468,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         f.pkey = c->f.pkey; f.pkey_alt = c->f.pkey_alt; f.pval = c->f.pval; f.pval_alt = c->f.pval_alt;
         f.gate = c->d_ctr;
         f.pair_cap = static_cast<unsigned long long>(c->p_cap);
-        launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
-        launches += n > 0;
+        launches += launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
         record(c, 4);
         // buckets > kBlendSortCap (sorted outside the blend): launched when the
         // last frame had any; a frame that has them unannounced is re-run
@@ -501,8 +506,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     uint32_t sort_cap = kBlendSortCapLarge;
     if (res.ctr.max_tile_len <= kMaxBucketSorted) {
         // K3: scatter splat indices into per-tile buckets
-        launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
-        launches += n > 0;
+        launches += launch_duplicate_buckets(f, P, n, c->d_ctr, strm);
         record(c, 4);
         // K4: exact (depth, index) order inside every bucket — long buckets
         // here, buckets of <= 1024 in the blend prologue (16x16 tiles), all of
@@ -518,6 +522,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     } else {
         // Fallback for tiles longer than one CTA's shared memory: global stable
         // radix sort by depth, duplicate in depth order, stable sort by tile.
+        f.tile_order = nullptr;
         bool oalt = radix_sort_u64(f.key, f.key_alt, f.val, f.val_alt, nullptr, n, 0, 64, c->radix_scratch,
                                    strm, &launches);
         order = oalt ? f.val_alt : f.val;
@@ -748,7 +753,7 @@ void ps_ctx_destroy(ps_ctx* c) {
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
     void* bufs[] = {c->n_block, c->p_block, c->radix_scratch, c->scan_scratch, c->img_rgb, c->img_t,
-                    c->f.flags, c->f.ranges, c->f.big_tiles, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage,
+                    c->f.flags, c->f.ranges, c->f.big_tiles, c->f.tile_order, c->cov_dbg, c->replay_vals, c->d_ctr, c->stage,
                     c->metrics_acc, c->cmp_block};
     for (void* b : bufs)
         if (b) cudaFree(b);

@@ -715,12 +715,93 @@ __device__ __noinline__ void duplicate_big(uint32_t* __restrict__ pval, uint32_t
             }
 }
 
+// Heavy-first tile order for the blend (its CTA -> tile map), so the long tiles
+// start in the first waves instead of trailing the grid: a counting sort of the
+// tiles by bucket length in 8-pair classes, run by one extra 256-thread CTA of
+// K3 (it finishes well inside K3; the blend follows K3 on the stream). Each
+// thread takes consecutive tiles as runs of equal class, one shared atomic per
+// run (neighbouring tiles mostly share a class; empty sky would otherwise
+// serialise on one bin).
+constexpr int kOrderBins = 512;
+constexpr int kOrderChunk = 16;
+static_assert(kOrderBins <= kWinCap, "the order bins reuse K3's window");
+
+__device__ __forceinline__ int order_bin(const uint2 r) {
+    return kOrderBins - 1 - static_cast<int>(min((r.y - r.x) >> 3, kOrderBins - 1u));
+}
+
+__device__ __noinline__ void build_tile_order(const uint2* __restrict__ ranges, int n_tiles,
+                                              uint32_t* __restrict__ order, uint32_t* obin) {
+    __shared__ uint32_t wsum[8];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int b = t; b < kOrderBins; b += 256) obin[b] = 0;
+    __syncthreads();
+    const int per = (n_tiles + 255) / 256;
+    const int t0 = min(n_tiles, t * per), t1 = min(n_tiles, t0 + per);
+    int cb = -1, ks = t0;
+    for (int c0 = t0; c0 < t1; c0 += kOrderChunk) {
+        int bin[kOrderChunk];
+#pragma unroll
+        for (int q = 0; q < kOrderChunk; ++q) bin[q] = c0 + q < t1 ? order_bin(ranges[c0 + q]) : -2;
+#pragma unroll
+        for (int q = 0; q < kOrderChunk; ++q)
+            if (bin[q] != cb && bin[q] != -2) {
+                if (cb >= 0) atomicAdd(&obin[cb], static_cast<uint32_t>(c0 + q - ks));
+                cb = bin[q];
+                ks = c0 + q;
+            }
+    }
+    if (cb >= 0) atomicAdd(&obin[cb], static_cast<uint32_t>(t1 - ks));
+    __syncthreads();
+    const uint32_t h0 = obin[2 * t], h1 = obin[2 * t + 1];
+    uint32_t x = h0 + h1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t pre = x - h0 - h1;
+    for (int w = 0; w < warp; ++w) pre += wsum[w];
+    obin[2 * t] = pre;
+    obin[2 * t + 1] = pre + h0;
+    __syncthreads();
+    auto flush = [&](int b, int k0, int k1) {
+        const uint32_t pos = atomicAdd(&obin[b], static_cast<uint32_t>(k1 - k0));
+        for (int k = k0; k < k1; ++k) order[pos + (k - k0)] = static_cast<uint32_t>(k);
+    };
+    cb = -1;
+    ks = t0;
+    for (int c0 = t0; c0 < t1; c0 += kOrderChunk) {
+        int bin[kOrderChunk];
+#pragma unroll
+        for (int q = 0; q < kOrderChunk; ++q) bin[q] = c0 + q < t1 ? order_bin(ranges[c0 + q]) : -2;
+#pragma unroll
+        for (int q = 0; q < kOrderChunk; ++q)
+            if (bin[q] != cb && bin[q] != -2) {
+                if (cb >= 0) flush(cb, ks, c0 + q);
+                cb = bin[q];
+                ks = c0 + q;
+            }
+    }
+    if (cb >= 0) flush(cb, ks, t1);
+}
+
 __global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n,
                                                                const DevCounters* __restrict__ ctr) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
     if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int blk = static_cast<int>(blockIdx.x);
+    if (f.tile_order) { // CTA 0 builds the blend's tile order
+        if (blk == 0) {
+            build_tile_order(f.ranges, P.tiles_x * P.tiles_y, f.tile_order, win);
+            return;
+        }
+        --blk;
+    }
+    const int64_t i = static_cast<int64_t>(blk) * blockDim.x + threadIdx.x;
     // all of a splat's inputs are loaded at once (one memory round trip; the
     // rect / mask / key of an inactive splat are stale and unused)
     const int64_t ic = i < n ? i : 0;
@@ -970,11 +1051,12 @@ void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* o
     k_duplicate<<<blocks, 256, 0, st>>>(f, P, order, n);
 }
 
-void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
-                              cudaStream_t st) {
-    if (n == 0) return;
-    const int blocks = static_cast<int>((n + 255) / 256);
+int launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
+                             cudaStream_t st) {
+    const int blocks = static_cast<int>((n + 255) / 256) + (f.tile_order ? 1 : 0);
+    if (blocks == 0) return 0;
     k_duplicate_buckets<<<blocks, 256, 0, st>>>(f, P, n, ctr);
+    return 1;
 }
 
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,

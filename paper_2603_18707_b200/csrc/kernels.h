@@ -36,8 +36,10 @@ void launch_scene_cov(const SceneDev& s, cudaStream_t st);
 void launch_duplicate(const FrameDev& f, const FrameParams& P, const uint32_t* order, int64_t n,
                       cudaStream_t st);
 // K3 also stores each entry's coarse depth key (tile_sort.cuh coarse_key) in f.pkey
-void launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
-                              cudaStream_t st);
+// and, when f.tile_order is set, builds the blend's heavy-first tile order
+// (one extra CTA). Returns the launches issued.
+int launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n, const DevCounters* ctr,
+                             cudaStream_t st);
 void launch_replay(const FrameDev& f, const FrameParams& P, DevCounters* ctr, float* out_rgb,
                    float* out_t, bool count_work, int sm_count, cudaStream_t st);
 
@@ -66,6 +68,7 @@ void launch_ranges(const uint32_t* keys, const uint32_t* d_n, int64_t n_cap, uin
 
 // binning.cu — per-tile buckets (K2 tile scan, K4 per-tile exact depth sort)
 // list_min: buckets longer than this go to the long-bucket list (sorted before the blend)
+constexpr int kTileOrderMax = 16384; // K3's order CTA: <= 64 tiles per thread
 void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
                       uint32_t list_min, cudaStream_t st);
 // sorts every bucket with 1 < length <= max_items (shared memory); returns false
