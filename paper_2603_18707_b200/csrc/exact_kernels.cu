@@ -302,6 +302,141 @@ __device__ __forceinline__ bool tile_rect_fast(double mx, double my, double cov_
     return true;
 }
 
+// Warp-cooperative tight tests for rects of up to 8x8 tiles. Rect sizes differ
+// a lot between the splats of a warp (1 to 64 tiles), so a per-thread loop runs
+// at the warp's largest rect. Instead each lane publishes its splat's fp32
+// screen (below) in shared memory, the warp enumerates all (splat, tile) tests
+// of its lanes in rounds of 32 (test g belongs to the first lane whose
+// inclusive prefix of rect sizes exceeds g), and each owner collects its
+// results from the round's ballot. Tests the fp32 screen cannot certify are
+// re-done by the owner with tight_test_fast's fp64 tiers.
+//   The screen is tight_test_fast's tier 1 with the box offsets formed as
+// fp32 fma(j, ts, fx0) (+ ts - 1) from the rect's first box offset fx0 =
+// fl(x0 - mx): two more fp32 roundings of offsets (<= ~4u32 relative), inside
+// the screen's ~170u32 scale margin. The centre-inside case (box minimum 0) is
+// decided exactly per splat: the one tile whose pixel-centre box holds the
+// centre, found with the reference's fp64 expressions.
+struct ScreenRec {
+    float a, b, c, kx, ky, q, fx0, fy0;
+    float rcpw;     // 1 / rect width (tile index -> row)
+    uint32_t meta;  // off (12 bits) | w << 12 | ix_in << 16 | iy_in << 20 | inside_pass << 24 | screen << 25
+    uint32_t pad[2];
+};
+
+__device__ __forceinline__ int inside_index(double m, int t0, int t1, int ts) {
+    // the tile t in [t0, t1] whose box [t ts + 0.5, t ts + ts - 0.5] holds m (else 15)
+    const int c = x86_cvtt_int(floor((m - 0.5) * (1.0 / ts))); // +-1 below: the estimate need not be exact
+#pragma unroll
+    for (int d = -1; d <= 1; ++d) {
+        const int t = c + d;
+        if (t < t0 || t > t1) continue;
+        const double x0 = t * static_cast<double>(ts) + 0.5;
+        const double bx1 = x0 + ts - 1;
+        if (x0 - m <= 0.0 && bx1 - m >= 0.0) return t - t0;
+    }
+    return 15;
+}
+
+__device__ __forceinline__ ScreenRec make_screen(const TightSplat& t, const int r[4], int ts, int off) {
+    ScreenRec s;
+    s.a = t.a32; s.b = t.b32; s.c = t.c32; s.kx = t.kx32; s.ky = t.ky32; s.q = t.q32;
+    s.fx0 = static_cast<float>((r[0] * static_cast<double>(ts) + 0.5) - t.mx);
+    s.fy0 = static_cast<float>((r[1] * static_cast<double>(ts) + 0.5) - t.my);
+    const int w = r[2] - r[0] + 1;
+    s.rcpw = 1.0f / static_cast<float>(w);
+    const int ixin = inside_index(t.mx, r[0], r[2], ts), iyin = inside_index(t.my, r[1], r[3], ts);
+    s.meta = static_cast<uint32_t>(off) | (static_cast<uint32_t>(w) << 12) | (static_cast<uint32_t>(ixin) << 16) |
+             (static_cast<uint32_t>(iyin) << 20) | ((0.0 <= t.qroot ? 1u : 0u) << 24) | ((t.screen ? 1u : 0u) << 25);
+    s.pad[0] = s.pad[1] = 0u;
+    return s;
+}
+
+// 1 = passes, 0 = fails, 2 = undecided (fp64 tiers)
+__device__ __forceinline__ int screen_test(const ScreenRec& s, int j, float tsf) {
+    const int w = static_cast<int>((s.meta >> 12) & 15u);
+    const int jy = static_cast<int>((static_cast<float>(j) + 0.5f) * s.rcpw);
+    const int jx = j - jy * w;
+    if (jx == static_cast<int>((s.meta >> 16) & 15u) && jy == static_cast<int>((s.meta >> 20) & 15u))
+        return (s.meta >> 24) & 1u;
+    if (!((s.meta >> 25) & 1u)) return 2;
+    const float flx = fmaf(static_cast<float>(jx), tsf, s.fx0), fhx = flx + (tsf - 1.0f);
+    const float fly = fmaf(static_cast<float>(jy), tsf, s.fy0), fhy = fly + (tsf - 1.0f);
+    auto q32 = [&](float dx, float dy) { return fmaf(s.a * dx, dx, fmaf(2.0f * s.b * dx, dy, s.c * dy * dy)); };
+    float m = q32(flx, fminf(fmaxf(s.kx * flx, fly), fhy));
+    m = fminf(m, q32(fhx, fminf(fmaxf(s.kx * fhx, fly), fhy)));
+    m = fminf(m, q32(fminf(fmaxf(s.ky * fly, flx), fhx), fly));
+    m = fminf(m, q32(fminf(fmaxf(s.ky * fhy, flx), fhx), fhy));
+    const float X = fmaxf(fabsf(flx), fabsf(fhx)), Y = fmaxf(fabsf(fly), fabsf(fhy));
+    const float scale = fabsf(s.a) * X * X + 2.0f * fabsf(s.b) * X * Y + fabsf(s.c) * Y * Y;
+    const float tol = fmaf(1e-5f, scale, fmaf(1e-6f, fabsf(s.q), 1e-30f));
+    if (scale < 1e30f) {
+        if (m < s.q - tol) return 1;
+        if (m > s.q + tol) return 0;
+    }
+    return 2;
+}
+
+// All lanes of the warp call this (converged). cand = this lane's rect size
+// (0: nothing to test), its screen already in srec[threadIdx.x] (offset field
+// 0; set here). Returns the
+// lane's pass bits in the stride-8 rect layout (bit 8 jy + jx) and, in *und,
+// the bits left undecided (same layout).
+__device__ __forceinline__ unsigned long long warp_tight_tests(ScreenRec* srec, int cand, int w, int h, float tsf,
+                                                               unsigned long long* und) {
+    const int lane = threadIdx.x & 31;
+    ScreenRec* wrec = srec + (threadIdx.x & ~31);
+    int inc = cand;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    const int off = inc - cand;
+    if (cand) wrec[lane].meta |= static_cast<uint32_t>(off);
+    __syncwarp();
+    unsigned long long pc = 0ull, uc = 0ull; // compact order (bit j)
+    for (int base = 0; base < total; base += 32) {
+        const int g = base + lane;
+        int owner = 0; // lanes whose inclusive prefix <= g
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, inc, owner + step - 1);
+            if (v <= g) owner += step;
+        }
+        int res = 0;
+        if (g < total) {
+            const ScreenRec& s = wrec[owner];
+            res = screen_test(s, g - static_cast<int>(s.meta & 0xfffu), tsf);
+        }
+        const uint32_t pb = __ballot_sync(0xffffffffu, res == 1);
+        const uint32_t ub = __ballot_sync(0xffffffffu, res == 2);
+        const int sh = off - base; // this lane's first test relative to the round
+        if (cand && sh < 32 && sh + cand > 0) {
+            if (sh >= 0) {
+                pc |= static_cast<unsigned long long>(pb >> sh);
+                uc |= static_cast<unsigned long long>(ub >> sh);
+            } else {
+                pc |= static_cast<unsigned long long>(pb) << (-sh);
+                uc |= static_cast<unsigned long long>(ub) << (-sh);
+            }
+        }
+    }
+    unsigned long long pm = 0ull, um = 0ull;
+    if (cand) {
+        const unsigned long long keep = cand == 64 ? ~0ull : ((1ull << cand) - 1ull);
+        pc &= keep;
+        uc &= keep;
+        const unsigned long long row = (1ull << w) - 1ull;
+        for (int jy = 0; jy < h; ++jy) {
+            pm |= ((pc >> (jy * w)) & row) << (8 * jy);
+            um |= ((uc >> (jy * w)) & row) << (8 * jy);
+        }
+    }
+    *und = um;
+    return pm;
+}
+
 // Block-level tile aggregation. Splats are Morton-ordered, so one CTA's splats
 // cover a compact screen region: per-tile counts / bucket slots are gathered
 // in a shared-memory window over the union of the CTA's tile rects, and only
@@ -415,11 +550,14 @@ template <int BC>
 __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
                                               double opacity, const FrameParams& P, const FrameDev& f,
                                               DevCounters* ctr, GeoOut* out = nullptr) {
+    __shared__ ScreenRec srec[256];
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
     bool small = false;
     unsigned long long my_mask = 0ull;
     int my_r[4] = {0, 0, -1, -1};
+    int cand = 0; // tiles of a small rect, tested by the warp below
+    const int ts = P.cfg.tile_size;
     if (in) {
         unsigned long long key = ~0ull;
         uint32_t cnt = 0;
@@ -436,31 +574,29 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                 raise_error(ctr, -b, i);
             } else if (b > 0) { // b == 0: below epsilon, dropped uncounted (raster.cpp:149-151)
                 int r[4];
-                const int ts = P.cfg.tile_size;
                 if (!tile_rect_fast(pr.mx, pr.my, pr.cov_aa.xx, pr.cov_aa.yy, radius, ts, P.cam.width, P.cam.height, r)) {
                     frustum = 1; // off screen (raster.cpp:165-168)
                 } else {
                     visible = 1;
                     coarse = static_cast<unsigned long long>(r[2] - r[0] + 1) *
                              static_cast<unsigned long long>(r[3] - r[1] + 1);
-                    unsigned long long mask = 0ull;
-                    const bool big = !rect_is_small(r);
                     const TightSplat tsp = make_tight(pr.conic, pr.mx, pr.my, qroot);
-                    for (int ty = r[1]; ty <= r[3]; ++ty)
-                        for (int tx = r[0]; tx <= r[2]; ++tx)
-                            if (tight_test_fast(tsp, tx, ty, ts)) {
-                                ++cnt;
-                                if (!big) mask |= 1ull << (((ty - r[1]) << 3) + (tx - r[0]));
-                                else if (f.tile_count) atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u);
-                            }
-                    small = !big && cnt > 0;
-                    my_mask = mask;
+                    if (!rect_is_small(r)) { // big rect (rare): per-thread tests, direct atomics
+                        for (int ty = r[1]; ty <= r[3]; ++ty)
+                            for (int tx = r[0]; tx <= r[2]; ++tx)
+                                if (tight_test_fast(tsp, tx, ty, ts)) {
+                                    ++cnt;
+                                    if (f.tile_count) atomicAdd(&f.tile_count[ty * P.tiles_x + tx], 1u);
+                                }
+                        f.tmask[i] = 0ull;
+                    } else {
+                        cand = static_cast<int>(coarse);
+                        srec[threadIdx.x] = make_screen(tsp, r, ts, 0);
+                    }
                     for (int k = 0; k < 4; ++k) my_r[k] = r[k];
-                    tight = cnt;
                     key = static_cast<unsigned long long>(__double_as_longlong(pr.depth));
                     kmin_inv = ~key;
                     kmax = key;
-                    f.tmask[i] = mask;
                     f.mean2d[i] = make_double2(pr.mx, pr.my);
                     f.conic_ab[i] = make_double2(pr.conic.xx, pr.conic.xy);
                     f.conic_cq[i] = make_double2(pr.conic.yy, qroot);
@@ -484,7 +620,29 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
         }
         f.key[i] = key;
         f.val[i] = static_cast<uint32_t>(i);
-        f.tcount[i] = cnt;
+        tight = cnt; // big rects; small ones below
+    }
+    {   // small rects: the warp's tests together (warp_tight_tests)
+        const int w = my_r[2] - my_r[0] + 1, h = my_r[3] - my_r[1] + 1;
+        unsigned long long und = 0ull;
+        unsigned long long mask = warp_tight_tests(srec, cand, w, h, static_cast<float>(ts), &und);
+        if (cand) {
+            if (und) { // the fp64 tiers for what the screen left open (rare)
+                const double2 mm = f.mean2d[i], ab = f.conic_ab[i], cq = f.conic_cq[i];
+                const TightSplat t = make_tight(Sym2{ab.x, ab.y, cq.x}, mm.x, mm.y, cq.y);
+                do {
+                    const int b = __ffsll(static_cast<long long>(und)) - 1;
+                    und &= und - 1;
+                    if (tight_test_fast(t, my_r[0] + (b & 7), my_r[1] + (b >> 3), ts)) mask |= 1ull << b;
+                } while (und);
+            }
+            const uint32_t cnt = static_cast<uint32_t>(__popcll(mask));
+            small = cnt > 0;
+            my_mask = mask;
+            f.tmask[i] = mask;
+            tight = cnt;
+        }
+        if (in) f.tcount[i] = static_cast<uint32_t>(tight);
     }
     if (f.tile_count) { // tight pairs per tile for the bucket scan (K2)
         __shared__ uint32_t win[kWinCap];
