@@ -946,7 +946,7 @@ __device__ __noinline__ void build_tile_order(const uint2* __restrict__ ranges, 
     if (cb >= 0) flush(cb, ks, t1);
 }
 
-__global__ void __launch_bounds__(256, 4) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n,
+__global__ void __launch_bounds__(256, 6) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n,
                                                                const DevCounters* __restrict__ ctr) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
