@@ -109,7 +109,7 @@ __device__ int blend_threshold_t(const ps_kernel& k, double o, double eps, doubl
 
 template <int BK>
 __device__ void blend_record(double a, double b, double c, double o, const FrameParams& P, float cr, float cg,
-                             float cb, float4& r0, float4& r1, float2& r2) {
+                             float cb, float4& r0, float4& r1, float2& r2, const double* qs_known = nullptr) {
     const double e32 = 5.9604644775390625e-08; // 2^-24
     const double e64 = 1.1102230246251565e-16; // 2^-53
     const ps_kernel& k = P.cfg.kernel;
@@ -118,7 +118,13 @@ __device__ void blend_record(double a, double b, double c, double o, const Frame
     double beta = b / a;
     double gamma = c - b * b / a;
     double qs = 0.0;
-    int th = blend_threshold_t<BK>(k, o, eps, qs);
+    int th;
+    if (qs_known) { // the culling bound's root is this threshold (same kernel, epsilon and opacity)
+        qs = *qs_known;
+        th = 1;
+    } else {
+        th = blend_threshold_t<BK>(k, o, eps, qs);
+    }
     float qhi, qlo, eT;
     bool ok = a > 0.0 && gamma > 0.0 && isfinite(beta) && isfinite(gamma);
     double amax = k.kind == PS_KERNEL_EXPONENTIAL ? o : o * k.coeffs[0];
@@ -498,7 +504,7 @@ enum BoundClass : int { kBcStp = 0, kBcZero = 1, kBcOaExp = 2, kBcOaP1 = 3, kBcO
 // culling_bound_for specialised per class. 1 = bound set, 0 = nullopt (below
 // epsilon, uncounted), -status on error. Same arithmetic as exact_math.cuh.
 template <int BC>
-__device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double& radius, double& qroot) {
+__device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double& radius, double& qroot, double& xr) {
     if (BC == kBcGeneric) return culling_bound_for(cfg, o, radius, qroot);
     if (!(o > 0.0)) return 0;
     double x = 0.0;
@@ -531,10 +537,20 @@ __device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double&
             if (st != PS_OK) return -st;
         }
     }
+    xr = x;
     qroot = x + kBoundSlack;
     radius = sqrt(qroot);
     return 1;
 }
+
+// The blend threshold (blend_threshold_t<BK>) of a visible splat equals the
+// culling root x of bound_for<BC> when both solve the same equation: the
+// opacity-aware bound of the blend kernel itself (no separate culling kernel),
+// or the exponential threshold 2 ln(o / eps) (StopThePop or opacity-aware exp).
+// The fused K1 then passes x on instead of solving it again.
+template <int BC, int BK>
+constexpr bool kThresholdIsBound = (BC == kBcOaP1 && BK == kBkP1) || (BC == kBcOaP2 && BK == kBkP2) ||
+                                   (BC == kBcOaP3 && BK == kBkP3) || ((BC == kBcOaExp || BC == kBcStp) && BK == kBkExp);
 
 // K1a for one view: splat i (in = i < n) with its camera-independent inputs
 // (mean, 3D covariance, opacity) already in registers. Every thread of the CTA
@@ -544,6 +560,7 @@ __device__ __forceinline__ int bound_for(const ps_config& cfg, double o, double&
 struct GeoOut {
     bool visible = false;
     double a = 0.0, b = 0.0, c = 0.0, o = 0.0; // conic (xx, xy, yy), opacity_eff
+    double x = 0.0;                             // the culling root (bound_for)
 };
 
 template <int BC>
@@ -568,8 +585,8 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
         } else if (st == 0) {
             frustum = 1; // kFrustum (raster.cpp:144-146,162-163)
         } else {
-            double radius = 0.0, qroot = 0.0;
-            const int b = bound_for<BC>(P.cfg, pr.opacity_eff, radius, qroot);
+            double radius = 0.0, qroot = 0.0, xr = 0.0;
+            const int b = bound_for<BC>(P.cfg, pr.opacity_eff, radius, qroot, xr);
             if (b < 0) {
                 raise_error(ctr, -b, i);
             } else if (b > 0) { // b == 0: below epsilon, dropped uncounted (raster.cpp:149-151)
@@ -609,6 +626,7 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                         out->b = pr.conic.xy;
                         out->c = pr.conic.yy;
                         out->o = pr.opacity_eff;
+                        out->x = xr;
                     }
                     if (f.cov_aa) {
                         f.cov_aa[3 * i] = pr.cov_aa.xx;
@@ -734,7 +752,7 @@ __global__ void __launch_bounds__(256, 3) k_geometry_mv(SceneDev s, MultiView<NV
 template <int BK>
 __device__ __forceinline__ void shade_record(int64_t i, const double (&mean)[3], const float (&v)[48],
                                              const FrameParams& P, const FrameDev& f, double ca, double cb, double cc,
-                                             double o) {
+                                             double o, const double* qs_known = nullptr) {
     // view direction (mean - camera position), normalised; fp32 suffices for colour
     const float dx = static_cast<float>(mean[0] - P.campos[0]);
     const float dy = static_cast<float>(mean[1] - P.campos[1]);
@@ -750,7 +768,7 @@ __device__ __forceinline__ void shade_record(int64_t i, const double (&mean)[3],
     }
     float4 r0, r1;
     float2 r2;
-    blend_record<BK>(ca, cb, cc, o, P, col[0], col[1], col[2], r0, r1, r2);
+    blend_record<BK>(ca, cb, cc, o, P, col[0], col[1], col[2], r0, r1, r2, qs_known);
     f.bl0[i] = r0;
     f.bl1[i] = r1;
     f.bl2[i] = r2;
@@ -803,7 +821,8 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev s, FrameParams P
     if (g.visible) {
         float v[48];
         load_sh<1>(s, i, P.sh_floats4, v);
-        shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o);
+        const bool same = kThresholdIsBound<BC, BK> && !P.cfg.has_culling_kernel;
+        shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o, same ? &g.x : nullptr);
     }
 }
 
