@@ -29,6 +29,8 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
                                                             uint32_t list_min) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t wmax[32];
+    pdl_trigger(); // K3 may be scheduled now (it waits for this scan)
+    pdl_wait();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t carry = 0, mx = 0;
     for (int base = 0; base < n_tiles; base += kScanThreads * kScanPer) {
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
                                                             int min_len_exclusive, const DevCounters* gate,
                                                             unsigned long long pair_cap) {
     extern __shared__ uint32_t smem[];
+    pdl_trigger();
+    pdl_wait();
     if (gate && gate->pairs_total > pair_cap) return;
     const uint32_t n = *count;
     for (uint32_t q = blockIdx.x; q < n; q += gridDim.x) {
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_list(const uint2* __restr
 
 void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
                       uint32_t list_min, cudaStream_t st) {
-    k_tile_scan<<<1, kScanThreads, 0, st>>>(tile_count, ranges, n_tiles, ctr, big_list, list_min);
+    launch_pdl(k_tile_scan, dim3(1), dim3(kScanThreads), 0, st, tile_count, ranges, n_tiles, ctr, big_list, list_min);
 }
 
 // Bucket length <= 1024: 128 threads per tile over all tiles; longer buckets
@@ -187,15 +191,18 @@ bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max
     if (max_len > kMaxBucketSorted && !unknown) return false;
     using S2 = TileSortSmem<512, 8>;
     cudaFuncSetAttribute(k_tile_sort_list<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S2::bytes()));
-    k_tile_sort_list<512, 8><<<148 * 4, 512, S2::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
-                                                               &d_ctr->big_tiles, static_cast<int>(cap), f.gate,
-                                                               f.pair_cap);
+    launch_pdl(k_tile_sort_list<512, 8>, dim3(148 * 4), dim3(512), S2::bytes(), st, f.ranges, f.pval,
+               static_cast<const uint32_t*>(f.pkey), static_cast<const unsigned long long*>(f.key), orig,
+               static_cast<const uint32_t*>(f.big_tiles), static_cast<const uint32_t*>(&d_ctr->big_tiles),
+               static_cast<int>(cap), f.gate, f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
         using S3 = TileSortSmem<1024, 12>;
         cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
-                                                                   &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
+        launch_pdl(k_tile_sort_list<1024, 12>, dim3(148), dim3(1024), S3::bytes(), st, f.ranges, f.pval,
+                   static_cast<const uint32_t*>(f.pkey), static_cast<const unsigned long long*>(f.key), orig,
+                   static_cast<const uint32_t*>(f.big_tiles), static_cast<const uint32_t*>(&d_ctr->big_tiles), 4096,
+                   f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
     return true;

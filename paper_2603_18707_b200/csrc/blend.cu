@@ -607,6 +607,7 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 template <int KIND, int ORDER, int MODE, bool COUNT, int CAPR>
 __global__ void __launch_bounds__(128, CAPR <= 12 ? 9 : 8) k_blend16(const BlendArgs A) {
     using SortSm = TileSortSmem<128, CAPR>;
+    pdl_wait(); // K3 / the long-bucket sorts
     // Shared memory: the bucket sort's workspace; the sorted list starts at word
     // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
     // overlay the sort's dead arrays below it. 9 CTAs (36 warps) per SM.
@@ -776,11 +777,11 @@ __global__ void __launch_bounds__(128, CAPR <= 12 ? 9 : 8) k_blend16(const Blend
 template <int KIND, int ORDER, int MODE>
 void launch16(const BlendArgs& a, int n_tiles, bool count, uint32_t cap, cudaStream_t st) {
     if (cap <= kBlendSortCapSmall) {
-        if (count) k_blend16<KIND, ORDER, MODE, true, kBlendSortCapSmall / 128><<<n_tiles, 128, 0, st>>>(a);
-        else k_blend16<KIND, ORDER, MODE, false, kBlendSortCapSmall / 128><<<n_tiles, 128, 0, st>>>(a);
+        if (count) launch_pdl(k_blend16<KIND, ORDER, MODE, true, kBlendSortCapSmall / 128>, dim3(n_tiles), dim3(128), 0, st, a);
+        else launch_pdl(k_blend16<KIND, ORDER, MODE, false, kBlendSortCapSmall / 128>, dim3(n_tiles), dim3(128), 0, st, a);
     } else {
-        if (count) k_blend16<KIND, ORDER, MODE, true, kBlendSortCapLarge / 128><<<n_tiles, 128, 0, st>>>(a);
-        else k_blend16<KIND, ORDER, MODE, false, kBlendSortCapLarge / 128><<<n_tiles, 128, 0, st>>>(a);
+        if (count) launch_pdl(k_blend16<KIND, ORDER, MODE, true, kBlendSortCapLarge / 128>, dim3(n_tiles), dim3(128), 0, st, a);
+        else launch_pdl(k_blend16<KIND, ORDER, MODE, false, kBlendSortCapLarge / 128>, dim3(n_tiles), dim3(128), 0, st, a);
     }
 }
 

@@ -96,6 +96,13 @@ struct FrameDev {
     unsigned long long pair_cap = ~0ull;
 };
 
+// Programmatic dependent launch (kernels.h launch_pdl): a dependent kernel may
+// be scheduled while its predecessor drains; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible (a no-op without
+// PDL), pdl_trigger() lets the dependent launch once every CTA has passed it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ bool pairs_overflow(const FrameDev& f) {
     return f.gate != nullptr && static_cast<unsigned long long>(f.gate->pairs_total) > f.pair_cap;
 }

@@ -818,6 +818,7 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev s, FrameParams P
     }
     GeoOut g;
     geometry_view<BC>(i, in, mean, c6, opacity, P, f, ctr, &g);
+    pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
     if (g.visible) {
         float v[48];
         load_sh<1>(s, i, P.sh_floats4, v);
@@ -969,6 +970,8 @@ __global__ void __launch_bounds__(256, 6) k_duplicate_buckets(FrameDev f, FrameP
                                                                const DevCounters* __restrict__ ctr) {
     __shared__ uint32_t win[kWinCap];
     __shared__ int wb[4];
+    pdl_trigger(); // the blend / long sorts may be scheduled into freed slots
+    pdl_wait();    // K2's cursors and key range
     if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
     int blk = static_cast<int>(blockIdx.x);
     if (f.tile_order) { // CTA 0 builds the blend's tile order
@@ -1232,7 +1235,7 @@ int launch_duplicate_buckets(const FrameDev& f, const FrameParams& P, int64_t n,
                              cudaStream_t st) {
     const int blocks = static_cast<int>((n + 255) / 256) + (f.tile_order ? 1 : 0);
     if (blocks == 0) return 0;
-    k_duplicate_buckets<<<blocks, 256, 0, st>>>(f, P, n, ctr);
+    launch_pdl(k_duplicate_buckets, dim3(blocks), dim3(256), 0, st, f, P, n, ctr);
     return 1;
 }
 

@@ -151,8 +151,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     }
     __syncthreads();
     uint32_t* list = hist;
-    int n_pad = 1;
-    while (n_pad < L) n_pad <<= 1;
+    const int n_pad = L > 1 ? 1 << (32 - __clz(L - 1)) : 1; // next power of two >= L
     if (need_bitonic && (n_pad > CAP || n_pad > (CAP > BINS ? CAP : BINS))) {
         // (cannot happen for power-of-two CAP; see above)
         for (int j = t; j < L; j += THREADS) list[j] = vin[j];
@@ -165,8 +164,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         for (int j = t; j < L; j += THREADS) list[j] = vin[j];
         __syncthreads();
         unsigned long long* fk = reinterpret_cast<unsigned long long*>(smem);
-        int n = 1;
-        while (n < L) n <<= 1;
+        const int n = n_pad;
         for (int j = t; j < n; j += THREADS) {
             if (j < L) fk[j] = key[list[j]];
             else { fk[j] = ~0ull; list[j] = 0xffffffffu; }
