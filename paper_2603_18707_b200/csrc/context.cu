@@ -437,7 +437,7 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     const uint32_t* order = nullptr;
     // heavy-first tile order for the blend, built by an extra CTA of K3 (render
     // frames through the bucketed path only; row-major otherwise)
-    if (req.mode != Mode::Render || n_tiles > kTileOrderMax) f.tile_order = nullptr;
+    if (req.mode != Mode::Render || !use_tile_order(n_tiles, n)) f.tile_order = nullptr;
     if (req.mode == Mode::Prepare) {
         // prepare_splats needs the global (depth, index) order: stable radix
         // sort of the fp64 depth bits (culled splats carry ~0 and sort last)

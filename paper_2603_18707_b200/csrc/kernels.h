@@ -88,7 +88,12 @@ void launch_ranges(const uint32_t* keys, const uint32_t* d_n, int64_t n_cap, uin
 
 // binning.cu — per-tile buckets (K2 tile scan, K4 per-tile exact depth sort)
 // list_min: buckets longer than this go to the long-bucket list (sorted before the blend)
-constexpr int kTileOrderMax = 16384; // K3's order CTA: <= 64 tiles per thread
+// K3's order CTA (one 256-thread CTA inside K3): used up to 16K tiles, or more
+// when K3 itself is long enough to hide it (>= 64 splats per tile)
+constexpr int kTileOrderMax = 16384;
+inline bool use_tile_order(int n_tiles, int64_t n) {
+    return n_tiles <= kTileOrderMax || static_cast<int64_t>(n_tiles) * 64 <= n;
+}
 void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCounters* ctr, uint32_t* big_list,
                       uint32_t list_min, cudaStream_t st);
 // sorts every bucket with 1 < length <= max_items (shared memory); returns false
