@@ -37,24 +37,25 @@ __device__ __forceinline__ void raise_error(DevCounters* ctr, int code, int64_t 
 // colour never feeds a discrete decision; its fp32 error (~1e-7) is inside the
 // image tolerance.
 __device__ void sh_color(const float* v, int degree, float x, float y, float z, float out[3]) {
+    // explicit fmaf: this file is compiled without FMA contraction (for the
+    // fp64 stages), and the colour needs no particular rounding order
+    float bs[16];
+    bs[0] = kSH0f;
+    bs[1] = -kSH1f * y; bs[2] = kSH1f * z; bs[3] = -kSH1f * x;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    bs[4] = kSH2f[0] * xy; bs[5] = kSH2f[1] * yz; bs[6] = kSH2f[2] * (2.0f * zz - xx - yy);
+    bs[7] = kSH2f[3] * xz; bs[8] = kSH2f[4] * (xx - yy);
+    bs[9] = kSH3f[0] * y * (3.0f * xx - yy); bs[10] = kSH3f[1] * xy * z;
+    bs[11] = kSH3f[2] * y * (4.0f * zz - xx - yy); bs[12] = kSH3f[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    bs[13] = kSH3f[4] * x * (4.0f * zz - xx - yy); bs[14] = kSH3f[5] * z * (xx - yy);
+    bs[15] = kSH3f[6] * x * (xx - yy);
+    const int nb = degree >= 3 ? 16 : degree == 2 ? 9 : degree == 1 ? 4 : 1;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-#define SH(k) v[3 * (k) + ch]
-        float c = SH(0) * kSH0f;
-        if (degree >= 1) c = c - SH(1) * (kSH1f * y) + SH(2) * (kSH1f * z) - SH(3) * (kSH1f * x);
-        if (degree >= 2) {
-            float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-            c = c + SH(4) * (kSH2f[0] * xy) + SH(5) * (kSH2f[1] * yz) +
-                SH(6) * (kSH2f[2] * (2.0f * zz - xx - yy)) + SH(7) * (kSH2f[3] * xz) +
-                SH(8) * (kSH2f[4] * (xx - yy));
-            if (degree >= 3)
-                c = c + SH(9) * (kSH3f[0] * y * (3.0f * xx - yy)) + SH(10) * (kSH3f[1] * xy * z) +
-                    SH(11) * (kSH3f[2] * y * (4.0f * zz - xx - yy)) +
-                    SH(12) * (kSH3f[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy)) +
-                    SH(13) * (kSH3f[4] * x * (4.0f * zz - xx - yy)) +
-                    SH(14) * (kSH3f[5] * z * (xx - yy)) + SH(15) * (kSH3f[6] * x * (xx - yy));
-        }
-#undef SH
+        float c = v[ch] * bs[0];
+#pragma unroll
+        for (int k = 1; k < 16; ++k)
+            if (k < nb) c = fmaf(v[3 * k + ch], bs[k], c);
         out[ch] = fmaxf(c + 0.5f, 0.0f);
     }
 }
