@@ -603,14 +603,15 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 }
 
 // CAPR: rounds of the prologue sort (12: buckets <= 1536 in 18 KB of shared
-// memory, 9 CTAs per SM; 16: <= 2048 in 24 KB, 8 CTAs per SM)
+// memory; 16: <= 2048 in 24 KB). 8 CTAs (32 warps) per SM at 64 registers:
+// measured faster than 9 at 56 (-5 us at C2) and 7 at 72 (+10 us)
 template <int KIND, int ORDER, int MODE, bool COUNT, int CAPR>
-__global__ void __launch_bounds__(128, CAPR <= 12 ? 9 : 8) k_blend16(const BlendArgs A) {
+__global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     using SortSm = TileSortSmem<128, CAPR>;
     pdl_wait(); // K3 / the long-bucket sorts
     // Shared memory: the bucket sort's workspace; the sorted list starts at word
     // SortSm::LIST, the staging records (a, b, c, d planes + coverage words)
-    // overlay the sort's dead arrays below it. 9 CTAs (36 warps) per SM.
+    // overlay the sort's dead arrays below it.
     __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];

@@ -33,7 +33,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 constexpr uint32_t kMaxBucketSorted = 12288u;
 // Longest bucket the blend kernel sorts in its prologue (16x16 tiles), chosen
 // per frame from the previous frame's longest bucket: 1536 (18 KB of shared
-// memory, 9 CTAs per SM) or 2048 (24 KB, 8 CTAs per SM); longer buckets are
+// memory) or 2048 (24 KB); longer buckets are
 // sorted by the list kernels (binning.cu) before the blend. K2 lists every
 // bucket longer than the smaller capacity.
 constexpr uint32_t kBlendSortCapSmall = 1536u;
