@@ -712,7 +712,7 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
 }
 
 template <int BC>
-__global__ void __launch_bounds__(256, 3) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
+__global__ void __launch_bounds__(256, 2) k_geometry(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = i < s.n;
     double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
