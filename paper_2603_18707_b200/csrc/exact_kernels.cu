@@ -332,9 +332,12 @@ struct ScreenRec {
 
 __device__ __forceinline__ int inside_index(double m, int t0, int t1, int ts) {
     // the tile t in [t0, t1] whose box [t ts + 0.5, t ts + ts - 0.5] holds m (else 15)
-    const int c = x86_cvtt_int(floor((m - 0.5) * (1.0 / ts))); // +-1 below: the estimate need not be exact
-#pragma unroll
-    for (int d = -1; d <= 1; ++d) {
+    // c = floor((m - 0.5) / ts): for a power-of-two ts the scaling is exact and
+    // rounding m - 0.5 is monotone with t ts and t ts + ts - 1 representable, so
+    // a centre in box t gives c == t; otherwise c +- 1 are tested too
+    const int c = x86_cvtt_int(floor((m - 0.5) * (1.0 / ts)));
+    const int span = (ts & (ts - 1)) == 0 ? 0 : 1;
+    for (int d = -span; d <= span; ++d) {
         const int t = c + d;
         if (t < t0 || t > t1) continue;
         const double x0 = t * static_cast<double>(ts) + 0.5;
