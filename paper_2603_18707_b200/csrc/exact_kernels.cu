@@ -347,16 +347,28 @@ __device__ __forceinline__ int inside_index(double m, int t0, int t1, int ts) {
     return 15;
 }
 
-__device__ __forceinline__ ScreenRec make_screen(const TightSplat& t, const int r[4], int ts, int off) {
+// The screen of a small-rect splat straight from its fp64 conic: the minimiser
+// multipliers kx = -b/c, ky = -b/a in fp32 (they only place the edge points,
+// so their error enters the box minimum at second order, like their rounding
+// from fp64 in make_tight); the fp64 ones are formed only for undecided tests.
+__device__ __forceinline__ ScreenRec make_screen(const Sym2& cn, double mx, double my, double qroot, const int r[4],
+                                                 int ts) {
     ScreenRec s;
-    s.a = t.a32; s.b = t.b32; s.c = t.c32; s.kx = t.kx32; s.ky = t.ky32; s.q = t.q32;
-    s.fx0 = static_cast<float>((r[0] * static_cast<double>(ts) + 0.5) - t.mx);
-    s.fy0 = static_cast<float>((r[1] * static_cast<double>(ts) + 0.5) - t.my);
+    s.a = static_cast<float>(cn.xx);
+    s.b = static_cast<float>(cn.xy);
+    s.c = static_cast<float>(cn.yy);
+    s.kx = s.c != 0.0f ? -s.b / s.c : 0.0f;
+    s.ky = s.a != 0.0f ? -s.b / s.a : 0.0f;
+    s.q = static_cast<float>(qroot);
+    const bool screen = s.a != 0.0f && s.c != 0.0f && fabsf(s.a) < 1e30f && fabsf(s.b) < 1e30f &&
+                        fabsf(s.c) < 1e30f && fabsf(s.kx) < 1e30f && fabsf(s.ky) < 1e30f && fabsf(s.q) < 1e30f;
+    s.fx0 = static_cast<float>((r[0] * static_cast<double>(ts) + 0.5) - mx);
+    s.fy0 = static_cast<float>((r[1] * static_cast<double>(ts) + 0.5) - my);
     const int w = r[2] - r[0] + 1;
     s.rcpw = 1.0f / static_cast<float>(w);
-    const int ixin = inside_index(t.mx, r[0], r[2], ts), iyin = inside_index(t.my, r[1], r[3], ts);
-    s.meta = static_cast<uint32_t>(off) | (static_cast<uint32_t>(w) << 12) | (static_cast<uint32_t>(ixin) << 16) |
-             (static_cast<uint32_t>(iyin) << 20) | ((0.0 <= t.qroot ? 1u : 0u) << 24) | ((t.screen ? 1u : 0u) << 25);
+    const int ixin = inside_index(mx, r[0], r[2], ts), iyin = inside_index(my, r[1], r[3], ts);
+    s.meta = (static_cast<uint32_t>(w) << 12) | (static_cast<uint32_t>(ixin) << 16) |
+             (static_cast<uint32_t>(iyin) << 20) | ((0.0 <= qroot ? 1u : 0u) << 24) | ((screen ? 1u : 0u) << 25);
     s.pad[0] = s.pad[1] = 0u;
     return s;
 }
@@ -601,8 +613,8 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                     visible = 1;
                     coarse = static_cast<unsigned long long>(r[2] - r[0] + 1) *
                              static_cast<unsigned long long>(r[3] - r[1] + 1);
-                    const TightSplat tsp = make_tight(pr.conic, pr.mx, pr.my, qroot);
                     if (!rect_is_small(r)) { // big rect (rare): per-thread tests, direct atomics
+                        const TightSplat tsp = make_tight(pr.conic, pr.mx, pr.my, qroot);
                         for (int ty = r[1]; ty <= r[3]; ++ty)
                             for (int tx = r[0]; tx <= r[2]; ++tx)
                                 if (tight_test_fast(tsp, tx, ty, ts)) {
@@ -612,7 +624,7 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                         f.tmask[i] = 0ull;
                     } else {
                         cand = static_cast<int>(coarse);
-                        srec[threadIdx.x] = make_screen(tsp, r, ts, 0);
+                        srec[threadIdx.x] = make_screen(pr.conic, pr.mx, pr.my, qroot, r, ts);
                     }
                     for (int k = 0; k < 4; ++k) my_r[k] = r[k];
                     key = static_cast<unsigned long long>(__double_as_longlong(pr.depth));
