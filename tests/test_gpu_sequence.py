@@ -1,0 +1,50 @@
+"""One context over a sequence of frames whose sizes change, as a viewer or a
+training loop would drive it. Frames after the first run speculatively (no
+mid-frame host sync, dependent launches, heavy-first tile order); the sequence
+makes them outgrow the previous frame's pair buffers (sized re-run), meet a
+bucket longer than the previous frame announced (re-run), an all-equal-depth
+bucket the prologue sort cannot pad (presorted re-run), and change the tile grid
+(buffers and tile order rebuilt) before shrinking again. Every frame against the
+reference: counters identical, images within 1e-5."""
+import pytest
+
+from paper_2603_18707_b200 import api
+from tests.helpers import camera, config, crowded_scene, max_abs, scene
+
+pytestmark = pytest.mark.gpu
+
+IMAGE_TOL = 1e-5
+
+# (kind, seed, n, width, height) or ("crowded", n, seed, same_depth)
+SEQUENCE = [
+    ("g", 1, 2000, 128, 96),
+    ("g", 1, 10000, 256, 256),   # more pairs than the first frame's buffers
+    ("crowded", 1500, 17, False),  # a bucket past the prologue sort, unannounced
+    ("g", 2, 50000, 640, 360),   # a larger tile grid
+    ("g", 1, 2000, 128, 96),
+    ("crowded", 1300, 16, True),   # equal depths: the presorted re-run
+    ("g", 2, 50000, 640, 360),
+    ("g", 1, 10000, 256, 256),
+]
+
+
+def _frame(item):
+    if item[0] == "crowded":
+        _, n, seed, same = item
+        return crowded_scene(n, seed, same)
+    kind, seed, n, w, h = item
+    splats, deg = scene(kind, seed, n)
+    return splats, deg, camera(1, w, h, 0)
+
+
+@pytest.mark.parametrize("kname,mode", [("poly1", api.CullingMode.OpacityAware), ("exp", api.CullingMode.StopThePop)])
+def test_changing_frame_sequence(reference, kname, mode):
+    with api.Rasterizer(0) as r:
+        for step, item in enumerate(SEQUENCE + SEQUENCE[::-1]):
+            splats, deg, cam = _frame(item)
+            cfg = config(kname, mode, deg)
+            rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+            fb, ctr = r.render(splats, cam, cfg)
+            assert ctr.as_dict() == ctr_r, (step, item)
+            assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL, (step, item)
+            assert max_abs(fb.transmittance, t_r) <= IMAGE_TOL, (step, item)
