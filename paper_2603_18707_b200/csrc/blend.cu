@@ -42,6 +42,7 @@ struct BlendArgs {
     uint32_t* flags;
     double4* replay_vals;              // exact (r, g, b, T) per replayed pixel (optional)
     DevCounters* ctr;
+    DevCounters* publish;              // pinned host copy of the counters (last CTA writes it), or null
     const DevCounters* gate;           // speculative frame: skip when pairs_total > pair_cap
     unsigned long long pair_cap;
     float* out_rgb;
@@ -605,6 +606,23 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 // CAPR: rounds of the prologue sort (12: buckets <= 1536 in 18 KB of shared
 // memory; 16: <= 2048 in 24 KB). 8 CTAs (32 warps) per SM at 64 registers:
 // measured faster than 9 at 56 (-5 us at C2) and 7 at 72 (+10 us)
+// The last CTA to finish copies the frame's counters to the host (mapped pinned
+// memory): every CTA's counter atomics are fenced before it counts itself done.
+__device__ __forceinline__ void publish_counters(const BlendArgs& A) {
+    if (!A.publish) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(&A.ctr->done_ctas, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x < sizeof(DevCounters) / 4) {
+        __threadfence();
+        const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(A.ctr);
+        reinterpret_cast<volatile uint32_t*>(A.publish)[threadIdx.x] = src[threadIdx.x];
+        __threadfence_system();
+    }
+}
+
 template <int KIND, int ORDER, int MODE, bool COUNT, int CAPR>
 __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     using SortSm = TileSortSmem<128, CAPR>;
@@ -623,7 +641,10 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kRecs); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
-    if (A.gate && A.gate->pairs_total > A.pair_cap) return; // over capacity: the host re-runs
+    if (A.gate && A.gate->pairs_total > A.pair_cap) { // over capacity: the host re-runs
+        publish_counters(A);
+        return;
+    }
     const FrameParams& P = A.P;
     const int tile = A.order ? static_cast<int>(A.order[blockIdx.x]) : static_cast<int>(blockIdx.x);
     const int tx = tile % P.tiles_x, ty = tile / P.tiles_x;
@@ -773,6 +794,7 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
             if (bl) atomicAdd(&A.ctr->blended, bl);
         }
     }
+    publish_counters(A);
 }
 
 template <int KIND, int ORDER, int MODE>
@@ -811,8 +833,9 @@ void launch_t(const BlendArgs& a, int n_tiles, int nt, size_t smem, bool count, 
 
 int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
                  uint32_t sort_cap, const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work,
-                 cudaStream_t st, bool* replay_fused) {
+                 cudaStream_t st, bool* replay_fused, DevCounters* publish, uint32_t* published) {
     *replay_fused = false;
+    if (published) *published = 0;
     BlendArgs a;
     a.P = P;
     a.ranges = f.ranges;
@@ -832,6 +855,7 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     a.flags = f.flags;
     a.replay_vals = f.replay_vals;
     a.ctr = ctr;
+    a.publish = nullptr;
     a.gate = f.gate;
     a.pair_cap = f.pair_cap;
     a.out_rgb = out.rgb;
@@ -842,6 +866,11 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     const int n_tiles = P.tiles_x * P.tiles_y;
     if (n_tiles == 0) return 0;
     if (ts == 16) {
+        if (publish && published) {
+            static_assert(sizeof(DevCounters) % 4 == 0 && sizeof(DevCounters) / 4 <= 128, "one word per thread");
+            a.publish = publish;
+            *published = static_cast<uint32_t>(n_tiles);
+        }
         if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, sort_cap, st);
         else launch16_kind<kAlphaThreshold>(a, n_tiles, count_work, sort_cap, st);
         *replay_fused = true; // flagged pixels are replayed inside k_blend16

@@ -58,6 +58,7 @@ struct DevCounters {
     unsigned long long key_max;
     unsigned int big_tiles;          // tiles with > 1024 pairs (listed in FrameDev::big_tiles)
     unsigned int unsorted;           // a blend-prologue bucket sort could not run (re-run presorted)
+    unsigned int done_ctas;          // blend CTAs finished (the last one publishes the counters to the host)
 };
 
 // Per-splat frame arrays (indexed by original splat index).

@@ -271,6 +271,7 @@ struct FrameResult {
     int64_t pairs = 0;
     bool pairs_in_alt = false;
     bool order_in_alt = false;
+    uint32_t published = 0;      // blend CTAs expected in h_ctr->done_ctas (0: counters copied instead)
     DevCounters ctr{};
 };
 
@@ -374,6 +375,8 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
                  const FrameRequest& req, FrameResult& res) {
     CTX_TRY(c, cudaStreamSynchronize(c->stream));
     CTX_TRY(c, cudaGetLastError());
+    if (res.published && c->h_ctr->done_ctas != res.published)
+        return set_err(c, PS_ERROR, "internal: the blend did not publish the frame counters");
     int st = check_frame_counters(c, s, res);
     if (st != PS_OK) return st;
     const uint32_t cap = blend_sort_cap(c->last_max_len); // what the speculative frame ran with
@@ -478,11 +481,13 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         record(c, 5);
         BlendOut out{req.d_rgb, req.d_t};
         bool replay_fused = false;
+        c->h_ctr->done_ctas = 0xffffffffu; // poisoned until the blend's last CTA publishes
         launches += launch_blend(f, P, f.pval, f.pval, cap, s->dev.orig, c->d_ctr, out, req.count_work, strm,
-                                 &replay_fused);
+                                 &replay_fused, c->h_ctr, &res.published);
         record(c, 6);
         record(c, 7);
-        CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
+        if (!res.published)
+            CTX_TRY(c, cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, strm));
         res.launches = launches;
         if (req.defer) return kPending; // finish_frame() syncs and checks
         return finish_frame(c, s, cam, cfg_in, req, res);

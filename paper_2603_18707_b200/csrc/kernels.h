@@ -108,9 +108,12 @@ struct BlendOut {
 };
 // sort_in_place: buckets of <= 1024 entries still unsorted (sorted in the blend
 // prologue and written back); null when every bucket is already sorted.
+// publish (16x16 tiles only): pinned host copy the blend's last CTA writes the
+// frame's counters to (no separate device-to-host copy); returns through
+// *published the CTA count it leaves in publish->done_ctas (0: not published).
 int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_vals, uint32_t* sort_in_place,
                  uint32_t sort_cap, const uint32_t* orig, DevCounters* ctr, BlendOut out, bool count_work,
-                 cudaStream_t st, bool* replay_fused);
+                 cudaStream_t st, bool* replay_fused, DevCounters* publish = nullptr, uint32_t* published = nullptr);
 // sort only buckets longer than min_len (the blend prologue handles the rest)
 bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max_len, uint32_t cap,
                            const DevCounters* d_ctr, cudaStream_t st, int* launches);
