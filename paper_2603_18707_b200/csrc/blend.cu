@@ -43,6 +43,7 @@ struct BlendArgs {
     double4* replay_vals;              // exact (r, g, b, T) per replayed pixel (optional)
     DevCounters* ctr;
     DevCounters* publish;              // pinned host copy of the counters (last CTA writes it), or null
+    uint32_t* zero_counts;             // with publish: per-tile counts, zeroed for the next frame
     const DevCounters* gate;           // speculative frame: skip when pairs_total > pair_cap
     unsigned long long pair_cap;
     float* out_rgb;
@@ -607,7 +608,8 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 // memory; 16: <= 2048 in 24 KB). 8 CTAs (32 warps) per SM at 64 registers:
 // measured faster than 9 at 56 (-5 us at C2) and 7 at 72 (+10 us)
 // The last CTA to finish copies the frame's counters to the host (mapped pinned
-// memory): every CTA's counter atomics are fenced before it counts itself done.
+// memory) and zeroes them for the next frame (which then needs no memset):
+// every CTA's counter atomics are fenced before it counts itself done.
 __device__ __forceinline__ void publish_counters(const BlendArgs& A) {
     if (!A.publish) return;
     __threadfence();
@@ -617,8 +619,9 @@ __device__ __forceinline__ void publish_counters(const BlendArgs& A) {
     __syncthreads();
     if (s_last && threadIdx.x < sizeof(DevCounters) / 4) {
         __threadfence();
-        const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(A.ctr);
+        volatile uint32_t* src = reinterpret_cast<volatile uint32_t*>(A.ctr);
         reinterpret_cast<volatile uint32_t*>(A.publish)[threadIdx.x] = src[threadIdx.x];
+        src[threadIdx.x] = 0u;
         __threadfence_system();
     }
 }
@@ -641,6 +644,7 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kRecs); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
+    if (A.zero_counts && threadIdx.x == 0) A.zero_counts[blockIdx.x] = 0u; // K3's cursors are dead
     if (A.gate && A.gate->pairs_total > A.pair_cap) { // over capacity: the host re-runs
         publish_counters(A);
         return;
@@ -856,6 +860,7 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     a.replay_vals = f.replay_vals;
     a.ctr = ctr;
     a.publish = nullptr;
+    a.zero_counts = nullptr;
     a.gate = f.gate;
     a.pair_cap = f.pair_cap;
     a.out_rgb = out.rgb;
@@ -869,6 +874,7 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
         if (publish && published) {
             static_assert(sizeof(DevCounters) % 4 == 0 && sizeof(DevCounters) / 4 <= 128, "one word per thread");
             a.publish = publish;
+            a.zero_counts = f.tile_count;
             *published = static_cast<uint32_t>(n_tiles);
         }
         if (P.threshold_mode == kQuadricThreshold) launch16_kind<kQuadricThreshold>(a, n_tiles, count_work, sort_cap, st);

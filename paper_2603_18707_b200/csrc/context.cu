@@ -59,6 +59,7 @@ struct ps_ctx {
     int64_t n_cap = 0;
     int64_t p_cap = 0;
     uint32_t last_max_len = 0; // longest bucket of the last rendered frame (speculation hint)
+    int64_t clean_tiles = 0;   // the last frame's blend left the counters and this many tile counts zero
     int64_t pix_cap = 0;
     int64_t tiles_cap = 0;
     FrameDev f;
@@ -238,6 +239,7 @@ int ensure_image(ps_ctx* c, int64_t pix, int n_tiles) {
         c->d_ctr = static_cast<DevCounters*>(blk);
         c->f.tile_count = reinterpret_cast<uint32_t*>(static_cast<char*>(blk) + kCtrBytes);
         c->tiles_cap = n_tiles;
+        c->clean_tiles = 0;
     }
     return PS_OK;
 }
@@ -392,6 +394,7 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
         return run_frame(c, s, cam, cfg_in, sized, res);
     }
     frame_stats(c, res);
+    c->clean_tiles = res.published; // the blend zeroed the counters and tile counts
     return PS_OK;
 }
 
@@ -427,9 +430,13 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
     cudaStream_t strm = c->stream;
     if (req.mode == Mode::Prepare) f.tile_count = nullptr;
     record(c, 0);
+    const bool clean = c->clean_tiles >= n_tiles && c->clean_tiles > 0;
+    c->clean_tiles = 0;
     if (!req.k1_done) {
-        // counters (+ the per-tile counts right after them) in one memset
-        CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, kCtrBytes + (f.tile_count ? sizeof(uint32_t) * n_tiles : 0), strm));
+        // counters (+ the per-tile counts right after them) in one memset,
+        // unless the last frame's blend left them zeroed
+        if (!clean)
+            CTX_TRY(c, cudaMemsetAsync(c->d_ctr, 0, kCtrBytes + (f.tile_count ? sizeof(uint32_t) * n_tiles : 0), strm));
         // K1: preprocess (+ tight pair count per tile)
         launches += launch_preprocess(s->dev, P, f, c->d_ctr, strm);
     }
