@@ -2,8 +2,9 @@
 (metrics.cpp:13-157, tools/main.cpp:300-345).
 
 Per-pixel terms are computed in the reference's fp64 operation order; only the
-sums over pixels are reduced in a different order, so psnr / ssim agree to
-~1e-12 relative on identical inputs and max_abs_diff is exact. compare() renders
+sums over pixels are reduced in a different (fixed) order, so psnr / ssim agree
+to ~1e-12 relative on identical inputs, are bit-reproducible from call to call,
+and max_abs_diff is exact. compare() renders
 with our rasterizer, whose images are within 1e-5 of the reference's, so its
 psnr / ssim are held to the tolerance that image error implies.
 """
@@ -42,6 +43,19 @@ def test_image_metrics_match_reference(gpu, reference, c1, dtype, bg):
     assert got.max_abs_diff == m
     assert math.isclose(got.psnr_db, p, rel_tol=1e-12)
     assert math.isclose(got.ssim, s, rel_tol=1e-12)
+
+
+def test_metrics_bit_reproducible(gpu, c1):
+    """The pixel sums are reduced in a fixed order: repeated calls (and a 1080p
+    image, whose SSIM tiles outnumber the grid) give the same bits."""
+    splats, deg, cam = c1
+    for w, h in ((256, 256), (1920, 1080)):
+        cam = camera(1, w, h, 0)
+        a, _ = gpu.render(splats, cam, config("exp", api.CullingMode.StopThePop, deg))
+        b, _ = gpu.render(splats, cam, config("poly1", api.CullingMode.OpacityAware, deg))
+        runs = [gpu.image_metrics(a, b) for _ in range(3)]
+        assert all((r.psnr_db, r.ssim, r.max_abs_diff) == (runs[0].psnr_db, runs[0].ssim, runs[0].max_abs_diff)
+                   for r in runs)
 
 
 def test_identical_images(gpu, c1):
