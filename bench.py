@@ -452,7 +452,7 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workl
 
 
 # stage -> kernel-name prefix in the ncu captures (blend: the 16x16 kernel of the headline kernel class)
-_STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0", "preprocess": "k_preprocess<3, 1>", "duplicate": "k_duplicate_buckets"}
+_STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0", "preprocess": "k_preprocess<3, 1, 3>", "duplicate": "k_duplicate_buckets"}
 
 
 def profiled_traffic(stage: str, kname: str, workload: str = "c2"):

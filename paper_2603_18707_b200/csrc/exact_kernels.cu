@@ -822,8 +822,9 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
 // pairs): the SH loads and colour of a visible splat follow its projection in
 // the same thread, so the HBM-bound SH traffic overlaps the fp64-latency-bound
 // geometry of other warps, and the conic / opacity stay in registers.
-template <int BC, int BK>
-__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
+// MINB: CTAs per SM the registers are budgeted for (3 at <= 1.5M splats, 2 above)
+template <int BC, int BK, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = i < s.n;
     double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
@@ -1159,14 +1160,16 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
                       cudaStream_t st) {
     if (s.n == 0) return 0;
     const int blocks = static_cast<int>((s.n + 255) / 256);
-    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323),
-    // for scenes whose frame arrays stay L2-resident: measured faster at 1M
-    // splats (182 vs 203 us) but slower from 2M on (383 vs 347 us at 2M, 1.33
-    // vs 1.02 ms at 6M), where the split K1a / K1b streams HBM better
-    constexpr int64_t kFusedMaxSplats = 1500000;
+    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323):
+    // 3 CTAs per SM (80 registers) up to 1.5M splats; above, 2 CTAs per SM
+    // (124 registers), which beats both the 3-CTA fused kernel and the split
+    // K1a / K1b there (C3 preprocess 1,026 -> 981 us, 2M: 340 -> 317 us) while
+    // losing at 1M (169 vs 191 us)
+    constexpr int64_t kFused3Max = 1500000;
 #define PS_FUSED(BCV, BKV)                                                                 \
-    if (s.n <= kFusedMaxSplats && P.bound_class == BCV && P.blend_class == BKV) {        \
-        k_preprocess<BCV, BKV><<<blocks, 256, 0, st>>>(s, P, f, ctr);                    \
+    if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
+        if (s.n <= kFused3Max) k_preprocess<BCV, BKV, 3><<<blocks, 256, 0, st>>>(s, P, f, ctr); \
+        else k_preprocess<BCV, BKV, 2><<<blocks, 256, 0, st>>>(s, P, f, ctr);           \
         return 1;                                                                        \
     }
     PS_FUSED(kBcStp, kBkExp)
