@@ -861,6 +861,32 @@ __global__ void __launch_bounds__(256) k_shade_mv(SceneDev s, MultiView<NV> mv) 
     for (int k = 0; k < NV; ++k) shade_view<BK>(i, mean, v, mv.P[k], mv.f[k]);
 }
 
+// Fused multi-view K1 (the common cells): each view's geometry, then the SH
+// coefficients loaded once and every view's colour / blend record, so the SH
+// stream overlaps the fp64 chains of other warps as in the single-view fused K1.
+template <int BC, int BK, int NV>
+__global__ void __launch_bounds__(256, 3) k_preprocess_mv(SceneDev s, MultiView<NV> mv) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = i < s.n;
+    double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
+    if (in) {
+        for (int k = 0; k < 3; ++k) mean[k] = s.mean[k][i];
+        for (int k = 0; k < 6; ++k) c6[k] = s.cov[k][i];
+        opacity = s.opacity[i];
+    }
+#pragma unroll 1
+    for (int v = 0; v < NV; ++v) geometry_view<BC>(i, in, mean, c6, opacity, mv.P[v], mv.f[v], mv.ctr[v]);
+    if (!in) return;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) any |= mv.f[k].key[i] != ~0ull;
+    if (!any) return;
+    float v[48];
+    load_sh<NV>(s, i, mv.P[0].sh_floats4, v);
+#pragma unroll 1
+    for (int k = 0; k < NV; ++k) shade_view<BK>(i, mean, v, mv.P[k], mv.f[k]);
+}
+
 // ------------------------------------------------------------ K3 duplicate
 // One thread per depth rank r: emits (tile id, splat index) for every tile of
 // the rect that passes the tight test, in the rect's row-major order, at the
@@ -1210,6 +1236,14 @@ void launch_mv(const SceneDev& s, const FrameParams* P, const FrameDev* f, DevCo
         mv.ctr[k] = ctr[k];
     }
     const int blocks = static_cast<int>((s.n + 255) / 256);
+    if (P[0].bound_class == kBcOaP1 && P[0].blend_class == kBkP1) {
+        k_preprocess_mv<kBcOaP1, kBkP1, NV><<<blocks, 256, 0, st>>>(s, mv);
+        return;
+    }
+    if (P[0].bound_class == kBcStp && P[0].blend_class == kBkExp) {
+        k_preprocess_mv<kBcStp, kBkExp, NV><<<blocks, 256, 0, st>>>(s, mv);
+        return;
+    }
     switch (P[0].bound_class) {
         case kBcStp: k_geometry_mv<kBcStp, NV><<<blocks, 256, 0, st>>>(s, mv); break;
         case kBcZero: k_geometry_mv<kBcZero, NV><<<blocks, 256, 0, st>>>(s, mv); break;
