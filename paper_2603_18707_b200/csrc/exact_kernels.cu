@@ -1186,16 +1186,16 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
                       cudaStream_t st) {
     if (s.n == 0) return 0;
     const int blocks = static_cast<int>((s.n + 255) / 256);
-    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323):
-    // 3 CTAs per SM (80 registers) up to 1.5M splats; above, 2 CTAs per SM
-    // (124 registers), which beats both the 3-CTA fused kernel and the split
-    // K1a / K1b there (C3 preprocess 1,026 -> 981 us, 2M: 340 -> 317 us) while
-    // losing at 1M (169 vs 191 us)
-    constexpr int64_t kFused3Max = 1500000;
+    // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323)
+    // up to 1.5M splats (3 CTAs per SM, 80 registers): at 1M 162 us against 191
+    // at 2 CTAs and 201 split. Above, the split K1a / K1b: in the bench's
+    // L2-flushed frames the fused kernel loses there (C3 preprocess 1,337 vs
+    // 1,004 us at 2 CTAs per SM, although back-to-back unflushed frames show it
+    // 5% ahead)
+    constexpr int64_t kFusedMax = 1500000;
 #define PS_FUSED(BCV, BKV)                                                                 \
-    if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
-        if (s.n <= kFused3Max) k_preprocess<BCV, BKV, 3><<<blocks, 256, 0, st>>>(s, P, f, ctr); \
-        else k_preprocess<BCV, BKV, 2><<<blocks, 256, 0, st>>>(s, P, f, ctr);           \
+    if (s.n <= kFusedMax && P.bound_class == BCV && P.blend_class == BKV) {              \
+        k_preprocess<BCV, BKV, 3><<<blocks, 256, 0, st>>>(s, P, f, ctr);                 \
         return 1;                                                                        \
     }
     PS_FUSED(kBcStp, kBkExp)
