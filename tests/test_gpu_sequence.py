@@ -48,3 +48,41 @@ def test_changing_frame_sequence(reference, kname, mode):
             assert ctr.as_dict() == ctr_r, (step, item)
             assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL, (step, item)
             assert max_abs(fb.transmittance, t_r) <= IMAGE_TOL, (step, item)
+
+
+def test_query_modes_interleaved_with_renders(reference):
+    """A context alternates renders (speculative after the first; each leaves the
+    counters and per-tile counts zeroed for the next frame) with pair counts,
+    tile lists, prepare_splats and view batches on different image sizes: every
+    result against the reference."""
+    splats, deg = scene("g", 1, 10000)
+    cfg = config("poly1", api.CullingMode.OpacityAware, deg)
+    big, small = camera(1, 256, 256, 0), camera(1, 96, 64, 0)
+
+    def check_render(r, cam):
+        rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+        fb, ctr = r.render(splats, cam, cfg)
+        assert ctr.as_dict() == ctr_r
+        assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
+
+    with api.Rasterizer(0) as r:
+        for cam in (big, big, small, big):
+            check_render(r, cam)
+            c = r.count_pairs(splats, cam, cfg).as_dict()
+            c_r = reference.count_pairs(splats, cam.to_struct(), cfg.to_struct())
+            assert c["tile_pairs_after_tight_test"] == c_r["tile_pairs_after_tight_test"]
+            assert c["tile_pairs_coarse"] == c_r["tile_pairs_coarse"]
+            check_render(r, cam)
+            off, idx, _ = r.tile_lists(splats, cam, cfg)
+            r_off, r_idx, _ = reference.tile_lists(splats, cam.to_struct(), cfg.to_struct())
+            assert (off == r_off).all() and (idx == r_idx).all()
+            check_render(r, cam)
+            got = r.prepare_splats(splats, cam, cfg)
+            ref = reference.prepare(splats, cam.to_struct(), cfg.to_struct())
+            assert (got.index == ref.index).all() and (got.depth == ref.depth).all()
+            check_render(r, cam)
+            cams = api.orbit_cameras(3, cam.width, cam.height)
+            for (fb, ctr), cv in zip(r.render_views(splats, cams, cfg), cams):
+                rgb_r, t_r, ctr_r = reference.render(splats, cv.to_struct(), cfg.to_struct())
+                assert ctr.as_dict() == ctr_r
+                assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL
