@@ -210,6 +210,8 @@ class Reference(_Lib):
         L.ref_synth_scene.argtypes = [C.c_int, C.c_uint64, C.POINTER(C.c_double), C.c_int64,
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int)]
         L.ref_synth_scene.restype = C.c_int
+        L.ref_synth_g.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.POINTER(C.c_double), C.c_int64]
+        L.ref_synth_g.restype = C.c_int
         L.ref_orbit_cameras.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_double, C.POINTER(abi.ps_camera)]
         L.ref_orbit_cameras.restype = C.c_int
@@ -237,6 +239,13 @@ class Reference(_Lib):
         out = np.zeros((n.value, abi.SPLAT3D_DOUBLES))
         self._call("synth_scene", kind, seed, dptr(out), n.value, C.byref(n), C.byref(deg))
         return out, deg.value
+
+    def synth_g(self, n: int, seed: int, skewed: bool = False):
+        """G(n, seed) (skewed: the C5 opacity law) as a Splat3D
+        array (n, 59), generated inside the reference library (ref_shim.cpp)."""
+        out = np.zeros((n, abi.SPLAT3D_DOUBLES))
+        self._call("synth_g", 4 if skewed else 3, seed, n, dptr(out), n)
+        return out, 3
 
     def orbit_cameras(self, count, width, height, fov_deg=50.0, radius=2.0, elevation=0.3):
         cams = (abi.ps_camera * count)()

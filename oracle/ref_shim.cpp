@@ -16,7 +16,9 @@
 #include "polysplat/reference.hpp"
 #include "polysplat/scene_io.hpp"
 
+#include <cmath>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -268,6 +270,53 @@ int ref_synth_scene(int kind, uint64_t seed, double* out, int64_t capacity, int6
         if (out) {
             if (static_cast<int64_t>(s.splats.size()) > capacity) return fail(PS_INVALID_ARGUMENT, "capacity too small");
             std::memcpy(out, s.splats.data(), s.splats.size() * sizeof(Splat3D));
+        }
+        return PS_OK;
+    });
+}
+
+// The parametric scene G(n, seed) of SURVEY §8d (kind 3) and its skewed-
+// opacity variant (kind 4, C5), written against the reference's Splat3D type
+// so the reference arm of bench.py needs no product code: the random-scene
+// distribution of scene_io.cpp:354-371 (same mt19937_64 uniform stream, same
+// draw order) with scales log-U(0.008 k, 0.045 k), k = (5000/n)^(1/3), and for
+// kind 4 opacity = 0.005 + 0.99 u^3. tests/test_oracle.py pins it bit for bit
+// against the product's generator (synth.cpp).
+int ref_synth_g(int kind, uint64_t seed, int64_t n, double* out, int64_t capacity) {
+    return guarded([&]() -> int {
+        if ((kind != 3 && kind != 4) || n <= 0) return fail(PS_INVALID_ARGUMENT, "kind must be 3 or 4, n > 0");
+        if (capacity < n) return fail(PS_INVALID_ARGUMENT, "capacity too small");
+        std::mt19937_64 gen(seed);
+        auto uni = [&]() { return double(gen() >> 11) * 0x1.0p-53; };
+        auto uab = [&](double a, double b) { return a + (b - a) * uni(); };
+        auto logu = [&](double a, double b) { return std::exp(uab(std::log(a), std::log(b))); };
+        const double pi = 3.141592653589793, sh0 = 0.28209479177387814;
+        const double k = std::cbrt(5000.0 / static_cast<double>(n));
+        const double lo = 0.008 * k, hi = 0.045 * k;
+        Splat3D* sp = reinterpret_cast<Splat3D*>(out);
+        for (int64_t i = 0; i < n; ++i) {
+            Splat3D s;
+            const double mx = uab(-0.5, 0.5), my = uab(-0.5, 0.5), mz = uab(-0.5, 0.5);
+            s.mean = {mx, my, mz};
+            const double sx = logu(lo, hi), sy = logu(lo, hi), sz = logu(lo, hi);
+            s.scale = {sx, sy, sz};
+            const double u1 = uni(), u2 = uni(), u3 = uni();
+            const double a = std::sqrt(1.0 - u1), b = std::sqrt(u1);
+            const double t2 = 2.0 * pi * u2, t3 = 2.0 * pi * u3;
+            s.rotation = Quat{b * std::cos(t3), a * std::sin(t2), a * std::cos(t2), b * std::sin(t3)};
+            if (kind == 4) {
+                const double u = uni();
+                s.opacity = 0.005 + 0.99 * u * u * u;
+            } else {
+                s.opacity = uab(0.05, 0.995);
+            }
+            const double r = uni(), g = uni(), bb = uni();
+            s.sh[0] = {(r - 0.5) / sh0, (g - 0.5) / sh0, (bb - 0.5) / sh0};
+            for (int j = 1; j < 16; ++j) {
+                const double x = uab(-0.04, 0.04), y = uab(-0.04, 0.04), z = uab(-0.04, 0.04);
+                s.sh[j] = {x, y, z};
+            }
+            sp[i] = s;
         }
         return PS_OK;
     });

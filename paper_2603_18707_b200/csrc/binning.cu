@@ -155,8 +155,8 @@ void launch_tile_scan(uint32_t* tile_count, uint2* ranges, int n_tiles, DevCount
 }
 
 // Bucket length <= 1024: 128 threads per tile over all tiles; longer buckets
-// (listed by k_tile_scan) by 512-thread (<= 4096) and 1024-thread (<= 12288)
-// CTAs. Longer than kMaxBucketSorted: returns false (caller falls back).
+// (listed by k_tile_scan) by 512-thread (<= 4096) and 1024-thread (<= 16384)
+// CTAs (power-of-two capacities: the bitonic fallback of sort_one_tile always fits). Longer than kMaxBucketSorted: returns false (caller falls back).
 bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint32_t max_len,
                       const DevCounters* d_ctr, cudaStream_t st, int* launches) {
     if (max_len <= 1 || n_tiles == 0) return true;
@@ -173,9 +173,9 @@ bool launch_tile_sort(const FrameDev& f, const uint32_t* orig, int n_tiles, uint
         if (launches) *launches += 1;
     }
     if (max_len > 4096u) {
-        using S3 = TileSortSmem<1024, 12>;
-        cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        k_tile_sort_list<1024, 12><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
+        using S3 = TileSortSmem<1024, 16>;
+        cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
+        k_tile_sort_list<1024, 16><<<148, 1024, S3::bytes(), st>>>(f.ranges, f.pval, f.pkey, f.key, orig, f.big_tiles,
                                                                    &d_ctr->big_tiles, 4096, f.gate, f.pair_cap);
         if (launches) *launches += 1;
     }
@@ -197,9 +197,9 @@ bool launch_tile_sort_long(const FrameDev& f, const uint32_t* orig, uint32_t max
                static_cast<int>(cap), f.gate, f.pair_cap);
     if (launches) *launches += 1;
     if (max_len > 4096u) {
-        using S3 = TileSortSmem<1024, 12>;
-        cudaFuncSetAttribute(k_tile_sort_list<1024, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
-        launch_pdl(k_tile_sort_list<1024, 12>, dim3(148), dim3(1024), S3::bytes(), st, f.ranges, f.pval,
+        using S3 = TileSortSmem<1024, 16>;
+        cudaFuncSetAttribute(k_tile_sort_list<1024, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S3::bytes()));
+        launch_pdl(k_tile_sort_list<1024, 16>, dim3(148), dim3(1024), S3::bytes(), st, f.ranges, f.pval,
                    static_cast<const uint32_t*>(f.pkey), static_cast<const unsigned long long*>(f.key), orig,
                    static_cast<const uint32_t*>(f.big_tiles), static_cast<const uint32_t*>(&d_ctr->big_tiles), 4096,
                    f.gate, f.pair_cap);

@@ -1,6 +1,7 @@
 // blend.cu — K6: front-to-back alpha blending per tile (raster.cpp:227-301).
 //
-// One CTA per tile, one pixel per thread (tile_size^2 <= 1024). The tile's
+// One CTA per tile, one pixel per thread (tile_size^2 <= 1024; larger tiles in
+// chunks of 1024 pixels). The tile's
 // splat list is staged through shared memory in batches of blockDim records
 // (gathered by splat index from the fp32 blend records written by K1, with the
 // fp64 mean turned into tile-local fp32 coordinates on the way in).
@@ -16,6 +17,8 @@
 // error bound on T; a pixel whose test value lands inside that band around the
 // floor is flagged and replayed exactly in fp64 by K7. Early termination: the CTA stops
 // when no pixel is live (__syncthreads_count), the reference's `remaining == 0`.
+#include <algorithm>
+
 #include "kernels.h"
 #include "tile_sort.cuh"
 
@@ -122,98 +125,106 @@ __global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
     const int W = P.cam.width, H = P.cam.height;
     const int px0 = tx * ts, py0 = ty * ts;
     const int t = threadIdx.x;
-    const int lx = t % ts, ly = t / ts;
-    const int gx = px0 + lx, gy = py0 + ly;
-    const bool inside = (t < ts * ts) && gx < W && gy < H;
-    const float xc = lx + 0.5f, yc = ly + 0.5f;
     const float eps = P.eps_f, floor_f = P.floor_f;
-
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, eT = 0.0f;
-    bool done = !inside, flagged = false;
-    uint32_t term = 0xffffffffu, nbl = 0, nexact = 0;
-
     const uint2 range = A.ranges[tile];
     const int L = static_cast<int>(range.y - range.x);
-    for (int base = 0; base < L; base += nt) {
-        if (__syncthreads_count(!done) == 0) break;
-        const int j = base + t;
-        if (j < L) {
-            const uint32_t i = A.pval[range.x + j];
-            const double2 m = A.mean2d[i];
-            const float4 b0 = A.bl0[i];
-            const float4 b1 = A.bl1[i];
-            const float2 b2 = A.bl2[i];
-            s0[t] = make_float4(static_cast<float>(m.x - px0), static_cast<float>(m.y - py0), b0.x, b0.y);
-            s1[t] = make_float4(b0.z, b0.w, b1.x, b1.y);
-            s2[t] = make_float4(b1.z, b1.w, b2.x, b2.y);
-            si[t] = i;
-        }
-        __syncthreads();
-        const int cnt = min(nt, L - base);
-        if (!done) {
-            for (int k = 0; k < cnt; ++k) {
-                const float4 v0 = s0[k];
-                const float4 v1 = s1[k];
-                const float dx = xc - v0.x, dy = yc - v0.y;
-                const float u = fmaf(v0.w, dy, dx);
-                const float q = fmaf(v0.z * u, u, v1.x * dy * dy);
-                float alpha;
-                if (MODE == kQuadricThreshold) {
-                    if (!(q <= v1.y)) continue; // alpha < eps certainly (or pixel/splat pair skipped)
-                    if (q >= v1.z) {            // inside the fp32 error band: decide in fp64
-                        ++nexact;
-                        if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+    unsigned long long ev = 0, bl = 0, ex = 0;
+
+    // Tiles of more than 1024 pixels (tile_size > 32, which the reference
+    // accepts: raster.cpp:13-23, 212-308) are blended in chunks of blockDim
+    // pixels, each walking the tile's whole list; one chunk otherwise.
+    const int npix = ts * ts;
+    for (int p0 = 0; p0 < npix; p0 += nt) {
+        const int p = p0 + t;
+        const int lx = p % ts, ly = p / ts;
+        const int gx = px0 + lx, gy = py0 + ly;
+        const bool inside = (p < npix) && gx < W && gy < H;
+        const float xc = lx + 0.5f, yc = ly + 0.5f;
+
+        float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, eT = 0.0f;
+        bool done = !inside, flagged = false;
+        uint32_t term = 0xffffffffu, nbl = 0, nexact = 0;
+
+        for (int base = 0; base < L; base += nt) {
+            if (__syncthreads_count(!done) == 0) break;
+            const int j = base + t;
+            if (j < L) {
+                const uint32_t i = A.pval[range.x + j];
+                const double2 m = A.mean2d[i];
+                const float4 b0 = A.bl0[i];
+                const float4 b1 = A.bl1[i];
+                const float2 b2 = A.bl2[i];
+                s0[t] = make_float4(static_cast<float>(m.x - px0), static_cast<float>(m.y - py0), b0.x, b0.y);
+                s1[t] = make_float4(b0.z, b0.w, b1.x, b1.y);
+                s2[t] = make_float4(b1.z, b1.w, b2.x, b2.y);
+                si[t] = i;
+            }
+            __syncthreads();
+            const int cnt = min(nt, L - base);
+            if (!done) {
+                for (int k = 0; k < cnt; ++k) {
+                    const float4 v0 = s0[k];
+                    const float4 v1 = s1[k];
+                    const float dx = xc - v0.x, dy = yc - v0.y;
+                    const float u = fmaf(v0.w, dy, dx);
+                    const float q = fmaf(v0.z * u, u, v1.x * dy * dy);
+                    float alpha;
+                    if (MODE == kQuadricThreshold) {
+                        if (!(q <= v1.y)) continue; // alpha < eps certainly (or pixel/splat pair skipped)
+                        if (q >= v1.z) {            // inside the fp32 error band: decide in fp64
+                            ++nexact;
+                            if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                        }
+                        alpha = alpha_f32<KIND>(q, v1.w, P.kf);
+                    } else {
+                        alpha = alpha_f32<KIND>(q, v1.w, P.kf);
+                        if (alpha < eps - v1.y) continue;
+                        if (alpha < eps + v1.y) {
+                            ++nexact;
+                            if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                        }
                     }
-                    alpha = alpha_f32<KIND>(q, v1.w, P.kf);
-                } else {
-                    alpha = alpha_f32<KIND>(q, v1.w, P.kf);
-                    if (alpha < eps - v1.y) continue;
-                    if (alpha < eps + v1.y) {
-                        ++nexact;
-                        if (!exact_alpha_ge_eps(P.cfg.kernel, P.cfg.epsilon, A.mean2d, A.conic_ab, A.conic_cq, A.opacity_eff, si[k], gx, gy)) continue;
+                    const float4 v2 = s2[k];
+                    // absolute error bound of the fp32 transmittance (see cand_step)
+                    const float om = 1.0f - alpha;
+                    const float test_t = T * om;
+                    const float en = fmaf(2.5f * 5.9604645e-08f, test_t, fmaf(eT, om, T * v2.x));
+                    if (test_t < floor_f + en) {
+                        done = true;
+                        if (test_t < floor_f - en) term = static_cast<uint32_t>(base + k);
+                        else flagged = true;
+                        break;
                     }
+                    eT = en;
+                    const float w = alpha * T;
+                    cr = fmaf(v2.y, w, cr);
+                    cg = fmaf(v2.z, w, cg);
+                    cb = fmaf(v2.w, w, cb);
+                    T = test_t;
+                    ++nbl;
                 }
-                const float4 v2 = s2[k];
-                // absolute error bound of the fp32 transmittance (see cand_step)
-                const float om = 1.0f - alpha;
-                const float test_t = T * om;
-                const float en = fmaf(2.5f * 5.9604645e-08f, test_t, fmaf(eT, om, T * v2.x));
-                if (test_t < floor_f + en) {
-                    done = true;
-                    if (test_t < floor_f - en) term = static_cast<uint32_t>(base + k);
-                    else flagged = true;
-                    break;
-                }
-                eT = en;
-                const float w = alpha * T;
-                cr = fmaf(v2.y, w, cr);
-                cg = fmaf(v2.z, w, cg);
-                cb = fmaf(v2.w, w, cb);
-                T = test_t;
-                ++nbl;
             }
         }
-    }
 
-    if (inside) {
-        const size_t pix = static_cast<size_t>(gy) * W + gx;
-        A.out_rgb[3 * pix + 0] = cr;
-        A.out_rgb[3 * pix + 1] = cg;
-        A.out_rgb[3 * pix + 2] = cb;
-        A.out_t[pix] = T;
-        if (flagged) {
-            const unsigned long long slot = atomicAdd(&A.ctr->replay_px, 1ull);
-            A.flags[slot] = static_cast<uint32_t>(pix);
+        if (inside) {
+            const size_t pix = static_cast<size_t>(gy) * W + gx;
+            A.out_rgb[3 * pix + 0] = cr;
+            A.out_rgb[3 * pix + 1] = cg;
+            A.out_rgb[3 * pix + 2] = cb;
+            A.out_t[pix] = T;
+            if (flagged) {
+                const unsigned long long slot = atomicAdd(&A.ctr->replay_px, 1ull);
+                A.flags[slot] = static_cast<uint32_t>(pix);
+            }
         }
+        // per-CTA sums of the reference's counters (raster.cpp:268,283); flagged
+        // pixels are counted by the exact replay instead
+        if (COUNT && inside && !flagged) {
+            ev += term != 0xffffffffu ? term + 1u : static_cast<unsigned>(L);
+            bl += nbl;
+        }
+        ex += nexact;
     }
-    // per-CTA sums of the reference's counters (raster.cpp:268,283); flagged
-    // pixels are counted by the exact replay instead
-    unsigned long long ev = 0, bl = 0;
-    if (COUNT && inside && !flagged) {
-        ev = term != 0xffffffffu ? term + 1u : static_cast<unsigned>(L);
-        bl = nbl;
-    }
-    unsigned long long ex = nexact;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         ev += __shfl_xor_sync(0xffffffffu, ev, o);
@@ -866,7 +877,8 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     a.out_rgb = out.rgb;
     a.out_t = out.t;
     const int ts = P.cfg.tile_size;
-    const int nt = ((ts * ts + 31) / 32) * 32;
+    // one pixel per thread up to 32x32 tiles; larger tiles in 1024-pixel chunks
+    const int nt = std::min(((ts * ts + 31) / 32) * 32, 1024);
     const size_t smem = static_cast<size_t>(nt) * (3 * sizeof(float4) + sizeof(uint32_t));
     const int n_tiles = P.tiles_x * P.tiles_y;
     if (n_tiles == 0) return 0;

@@ -292,8 +292,6 @@ int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode m
     ps_config cfg = cfg_in;
     if (cfg.sh_degree > 3) cfg.sh_degree = 3;
     if (cfg.sh_degree < 0) cfg.sh_degree = -1;
-    if ((mode == Mode::Render) && cfg.tile_size > 32)
-        return set_err(c, PS_INVALID_ARGUMENT, "device blend supports tile_size <= 32");
     if (cfg.kernel.kind != PS_KERNEL_EXPONENTIAL && (cfg.kernel.order < 1 || cfg.kernel.order > 3))
         return set_err(c, PS_INVALID_ARGUMENT, "kernel order must be in {1,2,3}");
     if (cfg.has_culling_kernel && cfg.culling_kernel.kind != PS_KERNEL_EXPONENTIAL &&
@@ -305,7 +303,10 @@ int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode m
     P.cfg = cfg;
     P.tiles_x = (cam.width + cfg.tile_size - 1) / cfg.tile_size;
     P.tiles_y = (cam.height + cfg.tile_size - 1) / cfg.tile_size;
-    const int sh_floats = cfg.sh_degree < 0 ? 0 : 3 * (cfg.sh_degree + 1) * (cfg.sh_degree + 1);
+    // the DC term is evaluated for every degree < 1, negative ones included
+    // (eval_sh_color, projection.cpp:93-95)
+    const int sh_deg = cfg.sh_degree < 0 ? 0 : cfg.sh_degree;
+    const int sh_floats = 3 * (sh_deg + 1) * (sh_deg + 1);
     P.sh_floats4 = (sh_floats + 3) / 4;
     P.threshold_mode = host_kernel_threshold_mode(cfg.kernel);
     P.kf.kind = cfg.kernel.kind;
@@ -667,7 +668,8 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
     CTX_TRY(c, cudaMemcpyAsync(st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
     CTX_TRY(c, cudaMemcpyAsync(st + 10 * n, opac, sizeof(double) * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(sh_st, sh, shb, kind, c->stream));
+    // exactly the caller's 48 n floats (shb only pads the staging layout)
+    CTX_TRY(c, cudaMemcpyAsync(sh_st, sh, sizeof(float) * 48 * static_cast<size_t>(n), kind, c->stream));
     launch_morton_order(st, n, bb, keys, vals, c->stream);
     const bool alt = radix_sort_u32(keys, keys_alt, vals, vals_alt, nullptr, n, 0, 30, scratch, c->stream, nullptr);
     launch_gather_scene(st, st + 10 * n, sh_st, alt ? vals_alt : vals, n, s->dev, c->stream);
@@ -1163,7 +1165,9 @@ namespace {
 
 // device buffers for two framebuffers (rgb + T) of `bytes_per_elem`-sized values
 int ensure_cmp(ps_ctx* c, int64_t pix, size_t elem) {
-    const size_t need = 2 * 4 * static_cast<size_t>(pix) * elem + 256;
+    // four 256-byte aligned regions (rgb a, T a, rgb b, T b; ps_image_metrics_compute)
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t need = 2 * al(3 * static_cast<size_t>(pix) * elem) + 2 * al(static_cast<size_t>(pix) * elem);
     if (!c->metrics_acc) CTX_TRY(c, cudaMalloc(&c->metrics_acc, ps::metrics_scratch_bytes()));
     if (need > c->cmp_bytes) {
         if (c->cmp_block) cudaFree(c->cmp_block);

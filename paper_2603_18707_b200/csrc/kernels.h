@@ -30,7 +30,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // Longest per-tile bucket sorted in shared memory (binning.cu); longer tiles
 // take the global radix-sort path.
-constexpr uint32_t kMaxBucketSorted = 12288u;
+constexpr uint32_t kMaxBucketSorted = 16384u;
 // Longest bucket the blend kernel sorts in its prologue (16x16 tiles), chosen
 // per frame from the previous frame's longest bucket: 1536 (18 KB of shared
 // memory) or 2048 (24 KB); longer buckets are

@@ -66,6 +66,10 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     constexpr int CAP = S::CAP, BINS = S::BINS, WARPS = S::WARPS, SH = S::BIN_SHIFT;
     constexpr int PER = BINS / THREADS;
     static_assert(BINS % (4 * THREADS) == 0 && CAP <= 65536, "tile sort shape");
+    // the list kernels (WRITEBACK) have no re-run path: their bitonic fallback
+    // must always fit, i.e. CAP a power of two (the blend prologue's 1536 flags
+    // *unsorted and its frame is re-run with every bucket presorted)
+    static_assert(!WRITEBACK || (CAP & (CAP - 1)) == 0, "list-kernel capacity must be a power of two");
     const uint32_t* vin = pval + r.x;                                 // bucket order (global)
     uint32_t* nk = smem;                                              // 32-bit key per bucket slot
     uint16_t* perm = reinterpret_cast<uint16_t*>(smem + CAP);          // bin-sorted position -> slot
@@ -153,7 +157,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
     uint32_t* list = hist;
     const int n_pad = L > 1 ? 1 << (32 - __clz(L - 1)) : 1; // next power of two >= L
     if (need_bitonic && (n_pad > CAP || n_pad > (CAP > BINS ? CAP : BINS))) {
-        // (cannot happen for power-of-two CAP; see above)
+        // (only the blend prologue's CAP 1536 gets here; it passes `unsorted`)
         for (int j = t; j < L; j += THREADS) list[j] = vin[j];
         if (t == 0 && unsorted) atomicExch(unsorted, 1u);
     } else if (!need_bitonic) {

@@ -1,6 +1,6 @@
 """GPU parity on crowded tiles (tests/helpers.crowded_scene): buckets longer than
 the blend prologue's shared-memory sort (1536), the 512-thread list sort (4096),
-the 1024-thread list sort (12288, beyond which the global radix path runs), and
+the 1024-thread list sort (16384, beyond which the global radix path runs), and
 all-equal depths (tie order by splat index, bitonic path; a prologue bucket of
 1024-1536 equal depths cannot be padded to 2048 in shared memory, so the frame
 is re-run with every bucket presorted). Each scene is rendered twice: the
@@ -15,7 +15,7 @@ from tests.helpers import config, crowded_scene, max_abs
 pytestmark = pytest.mark.gpu
 
 CASES = [(700, 11, True), (1300, 16, True), (1500, 17, False), (3000, 12, False), (6000, 13, False),
-         (20000, 14, False), (2500, 15, True)]
+         (20000, 14, False), (2500, 15, True), (10000, 18, True), (15000, 19, False), (15000, 20, True)]
 CELLS = [("poly1/opacity", "poly1", api.CullingMode.OpacityAware), ("exp/stp", "exp", api.CullingMode.StopThePop)]
 
 

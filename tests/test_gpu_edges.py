@@ -21,7 +21,7 @@ def _check(gpu, reference, splats, cam, cfg):
     return fb, ctr
 
 
-@pytest.mark.parametrize("tile", [8, 12, 32])
+@pytest.mark.parametrize("tile", [1, 8, 12, 32, 33, 48, 64, 100])
 @pytest.mark.parametrize("kname,mode", [("poly1", api.CullingMode.OpacityAware), ("exp", api.CullingMode.StopThePop)])
 def test_other_tile_sizes(gpu, reference, tile, kname, mode):
     splats, deg = scene("random", 3)

@@ -215,3 +215,20 @@ def test_golden_fixtures(restatement):
         assert [ctr[k] for k in sorted(ctr)] == list(g[key + "_ctr"]), key
         off, idx, _ = restatement.tile_lists(splats, cam, cfg)
         assert np.array_equal(off, g[key + "_off"]) and np.array_equal(idx, g[key + "_idx"]), key
+
+
+@pytest.mark.parametrize("skewed", [False, True], ids=["g", "skewed"])
+def test_reference_side_generator_matches_product(reference, skewed):
+    """G(n, seed) generated inside the reference library (the bench's reference
+    arm uses it, so that arm maps no product code) is bit-identical to the
+    product's synth.cpp generator."""
+    from paper_2603_18707_b200 import api
+    a, _ = reference.synth_g(5000, 11, skewed)
+    b, _ = api.synthetic_splat3d(4 if skewed else 3, 11, 5000)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    cams_r = reference.orbit_cameras(8, 1920, 1080)
+    cams_p = api.orbit_cameras(8, 1920, 1080)
+    for cr, cp in zip(cams_r, cams_p):
+        s = cp.to_struct()
+        assert list(cr.rotation) == list(s.rotation) and list(cr.translation) == list(s.translation)
+        assert (cr.fx, cr.fy, cr.cx, cr.cy) == (s.fx, s.fy, s.cx, s.cy)
