@@ -5,11 +5,23 @@
 
 A step renders one 1920x1080 frame of the C2 scene (G(1M, seed 2), SH degree 3,
 fitted poly-1 kernel with opacity-aware culling) through ps_render with the scene
-resident in HBM. Under torchrun (N > 1) every rank renders its own orbit view of
-a replicated scene (view sharding, no data-path collective; "scaling": "weak");
-timing is CUDA events on the rasterizer's stream, barrier + max over ranks.
+resident in HBM (counters off, device outputs: the instantiation
+tests/test_gpu_timed_path.py checks against the reference). Under torchrun
+(N > 1) every rank renders its own orbit view of a replicated scene each step
+(view sharding, no data-path collective; "scaling": "weak"); timing is CUDA
+events on the rasterizer's stream, barrier + max over ranks. The line also
+carries: the timed frame's parity against the reference's image of the same
+frame, the stage split and roofline, the reference's ablation cells with device
+times (tools/main.cpp:315-323 + the paper's f'2/S row), the C5 culling ablation,
+the C4 256-view batch sharded over the ranks (strong scaling), the end-to-end
+rate through the C ABI with host buffers (pinned SoA scene upload, and the
+literal drop-in ps_render_splats with a host Splat3D array), and the
+reference's own CPU renderer timed on this host.
+
 `--impl reference` times the reference's own CPU renderer (oracle/_ref, the
-unmodified reference library built from source) on the same workload, rank 0 only.
+unmodified reference library built from source) on the same workload, rank 0
+only; its inputs come from the reference library too (ref_synth_g /
+orbit_cameras), so that arm maps no product code.
 """
 from __future__ import annotations
 
@@ -19,7 +31,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -36,11 +47,16 @@ WORKLOADS = {
     "c5": ("skewed", 3, 1_000_000, 1920, 1080, 1),
 }
 HEADLINE = ("poly1/opacity", "poly1", "OpacityAware")
-COMPARE = [("exp/stp", "exp", "StopThePop"), ("poly1/zero", "poly1", "ZeroCrossing"),
-           ("poly2p/opacity", "poly2p", "OpacityAware"), ("poly3/opacity", "poly3", "OpacityAware")]
+# the reference CLI's ablation cells (tools/main.cpp:315-323) + the paper's
+# f'2/S row; each is timed on the C2 frame
+ABLATION = [("exp/stp", "exp", "StopThePop"), ("poly1/stp", "poly1", "StopThePop"),
+            ("poly1/zero", "poly1", "ZeroCrossing"), ("poly1/opacity", "poly1", "OpacityAware"),
+            ("poly2p/stp", "poly2p", "StopThePop"), ("poly2p/opacity", "poly2p", "OpacityAware"),
+            ("poly3/stp", "poly3", "StopThePop"), ("poly3/opacity", "poly3", "OpacityAware")]
 # FP32 lane-instructions per kernel evaluation / per blended fragment
 OPS_PER_EVAL = {"poly1": 6, "poly2p": 8, "poly3": 8, "exp": 7, "poly2": 8}
 OPS_PER_BLEND = 6
+SPLAT3D_BYTES = 59 * 8
 
 
 def peaks() -> dict:
@@ -49,6 +65,17 @@ def peaks() -> dict:
             return json.load(fh)
     except OSError:
         return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -99,24 +126,39 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def make_cfg(api, kname: str, mode: str, sh_degree: int):
-    return api.RasterConfig(kernel=api.fitted_kernel(kname), culling_mode=getattr(api.CullingMode, mode),
-                            sh_degree=sh_degree)
+def workload_config(name: str) -> dict:
+    """The `config` of both arms' lines (identical dicts)."""
+    kind, seed, n, w, h, views = WORKLOADS[name]
+    return {"workload": f"{name.upper()}: synthetic G({n}, seed {seed}{', skewed opacity' if kind == 'skewed' else ''}), "
+                        f"{w}x{h}, SH degree 3, {HEADLINE[0]} (fitted poly-1, opacity-aware bound)",
+            "gaussians": n, "width": w, "height": h, "kernel": HEADLINE[0], "parallelism": "view-sharded",
+            "views_per_rank_per_step": 1,
+            "l2": "flushed between timed steps (256 MiB write); scene (280 MB) also exceeds the 126 MB L2"}
+
+
+def _scene_key(kind: str) -> int:
+    return {"g": 3, "skewed": 4}[kind]
 
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args) -> None:
+    """The reference's own CPU renderer (oracle/_ref), rank 0 only. Inputs from
+    the reference library itself (ref_synth_g, the reference's orbit_cameras):
+    nothing of the product is loaded in this process."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import oracle  # the reference's own CPU renderer (oracle/_ref)
-    from paper_2603_18707_b200 import api
+    from oracle import oracle
+    from paper_2603_18707_b200 import abi
 
     kind, seed, n, w, h, _ = WORKLOADS[args.workload]
     ref = oracle.Reference()
-    splats, deg = api.synthetic_splat3d({"g": 3, "skewed": 4}[kind], seed, n)
-    cam = api.orbit_cameras(256, w, h)[0].to_struct()
-    cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg).to_struct()
+    splats, deg = ref.synth_g(n, seed, kind == "skewed")
+    cam = ref.orbit_cameras(256, w, h)[0]
+    cfg = abi.default_config()
+    cfg.kernel = ref.make_polynomial_kernel(abi.PS_KERNEL_POLY_RELU, (0.77007333317642512, -0.17527402122331368))
+    cfg.culling_mode = abi.PS_CULL_OPACITY_AWARE
+    cfg.sh_degree = deg
     for _ in range(args.warmup):
         ref.render(splats, cam, cfg)
     times = []
@@ -133,7 +175,8 @@ def run_reference(args) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload),
         "gaussians_per_s": fps * n,
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference",
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "cpu_model": cpu_model(),
+                         "kind": "reference",
                          "sample": f"{args.steps} full frames of {args.workload} ({HEADLINE[0]}) via "
                                    "polysplat::render, OpenMP over all host threads"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -141,270 +184,366 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def workload_config(name: str) -> dict:
-    kind, seed, n, w, h, views = WORKLOADS[name]
-    return {"workload": f"{name.upper()}: synthetic G({n}, seed {seed}{', skewed opacity' if kind == 'skewed' else ''}), "
-                        f"{w}x{h}, SH degree 3, {HEADLINE[0]} (fitted poly-1, opacity-aware bound)",
-            "gaussians": n, "width": w, "height": h, "kernel": HEADLINE[0], "parallelism": "view-sharded",
-            "l2": "flushed between timed steps (256 MiB write); scene (280 MB) also exceeds the 126 MB L2"}
-
-
 # ---------------------------------------------------------------------------- our arm
-def run_ours(args) -> None:
-    import numpy as np
-    import torch
+class Ours:
+    """One rank's rasterizer, scene and timing helpers."""
 
-    from paper_2603_18707_b200 import api
+    def __init__(self, args):
+        import torch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2603_18707_b200 import api
+        self.torch, self.api = torch, api
+        self.args = args
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        self.lib = api.lib()
+        self.r = api.Rasterizer(self.local)
+        self.stream = torch.cuda.ExternalStream(self.lib.ps_ctx_stream(self.r.handle),
+                                                device=torch.device("cuda", self.local))
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    from paper_2603_18707_b200.sharding import max_over_ranks, shard_views
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
 
-    kind, seed, n, w, h, nviews = WORKLOADS[args.workload]
-    scene = api.Scene.synthetic(kind, seed, n)
-    deg = scene.sh_degree
-    cams = api.orbit_cameras(nviews, w, h)
-    if args.workload == "c4":
-        # C4: the 256-view batch sharded across ranks every step (scene replicated)
-        my_views = list(shard_views(nviews, world, rank))
-    else:
-        # one view per rank per step (weak scaling); rank 0 renders orbit view 0
-        my_views = [(rank * max(1, nviews // max(world, 1))) % nviews]
-    cam = cams[my_views[0]]
-    frames_per_step = len(my_views)
-    r = api.Rasterizer(local)
-    ds = r.upload(scene)
-    lib = api.lib()
-    import ctypes as C
-    stream = torch.cuda.ExternalStream(lib.ps_ctx_stream(r.handle), device=torch.device("cuda", local))
-    out_rgb = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
-    out_t = torch.empty((h, w), dtype=torch.float32, device="cuda")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    cam_s = cam.to_struct()
+    def max_ms(self, ms: float) -> float:
+        from paper_2603_18707_b200.sharding import max_over_ranks
+        return max_over_ranks(ms, self.dist, device="cuda")
 
-    cam_structs = [cams[v].to_struct() for v in my_views]
-    # several views per step: one ps_render_views call (K1 fused over batches of
-    # views, each view's binning / blend on its own stream) into per-view outputs
-    batch = len(cam_structs) > 1
-    if batch:
-        cam_arr = (type(cam_structs[0]) * len(cam_structs))(*cam_structs)
-        out_rgb = torch.empty((len(cam_structs), h, w, 3), dtype=torch.float32, device="cuda")
-        out_t = torch.empty((len(cam_structs), h, w), dtype=torch.float32, device="cuda")
+    def cfg(self, kname: str, mode: str, deg: int):
+        api = self.api
+        return api.RasterConfig(kernel=api.fitted_kernel(kname), culling_mode=getattr(api.CullingMode, mode),
+                                sh_degree=deg)
 
-    def render_dev(cfg_s):
-        if batch:
-            st = lib.ps_render_views(r.handle, ds.handle, cam_arr, len(cam_structs), C.byref(cfg_s),
-                                     out_rgb.data_ptr(), out_t.data_ptr(), 1, None)
-            if st != 0:
-                raise RuntimeError(api.last_error(r.handle))
-            return
-        for cs in cam_structs:
+    def render_fn(self, ds, cam_structs, cfg_s, out_rgb, out_t):
+        """One step's call: ps_render per view (one view) or ps_render_views
+        (a batch), counters NULL, device outputs."""
+        import ctypes as C
+        lib, r, api = self.lib, self.r, self.api
+        if len(cam_structs) > 1:
+            arr = (type(cam_structs[0]) * len(cam_structs))(*cam_structs)
+
+            def go():
+                st = lib.ps_render_views(r.handle, ds.handle, arr, len(cam_structs), C.byref(cfg_s),
+                                         out_rgb.data_ptr(), out_t.data_ptr(), 1, None)
+                if st != 0:
+                    raise RuntimeError(api.last_error(r.handle))
+            return go
+        cs = cam_structs[0]
+
+        def go1():
             st = lib.ps_render(r.handle, ds.handle, C.byref(cs), C.byref(cfg_s), out_rgb.data_ptr(),
                                out_t.data_ptr(), 1, None)
             if st != 0:
                 raise RuntimeError(api.last_error(r.handle))
+        return go1
 
-    def timed(cfg_s, steps, warmup, sample_clocks=False):
+    def timed(self, fn, steps: int, warmup: int, sample_clocks: bool = False):
+        """W untimed steps, then K steps each bracketed by CUDA events on the
+        rasterizer's stream with an L2 flush before it; barrier + sync on both
+        sides; mean ms per step, max over ranks; kernel launches counted."""
+        torch = self.torch
         for _ in range(warmup):
-            render_dev(cfg_s)
-        # the timed steps run without per-stage events (events between the
-        # kernels would serialise the programmatic dependent launches); the
-        # stage split comes from separate frames below
-        r.set_timing(False)
+            fn()
+        self.r.set_timing(False)  # no per-stage events inside the timed steps
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         launches = 0
-        if dist:
-            dist.barrier()
+        self.barrier()
         torch.cuda.synchronize()
-        sampler = ClockSampler(local) if sample_clocks else None
+        sampler = ClockSampler(self.local) if sample_clocks else None
         if sampler:
             sampler.__enter__()
         for k in range(steps):
-            flush.zero_()
+            self.flush.zero_()
             torch.cuda.synchronize()
-            evs[k][0].record(stream)
-            render_dev(cfg_s)
-            evs[k][1].record(stream)
-            launches += r.stats()["kernel_launches"]
+            evs[k][0].record(self.stream)
+            fn()
+            evs[k][1].record(self.stream)
+            launches += self.r.stats()["kernel_launches"]
         torch.cuda.synchronize()
+        self.barrier()
         if sampler:
             sampler.__exit__(None, None, None)
         ms = sum(a.elapsed_time(b) for a, b in evs) / steps
-        ms = max_over_ranks(ms, dist, device="cuda")
-        # per-stage split (per frame; a batched step reports its views' summed
-        # stage times) from a few more flushed steps with stage events
-        r.set_timing(True)
-        stage_sum, reps = {}, max(3, min(steps, 20))
+        return self.max_ms(ms), launches, (sampler.summary() if sampler else None)
+
+    def stage_split(self, fn, reps: int, views: int = 1) -> dict:
+        """Per-frame stage times (ms) from separate flushed frames with stage events."""
+        torch = self.torch
+        self.r.set_timing(True)
+        acc = {}
         for _ in range(reps):
-            flush.zero_()
+            self.flush.zero_()
             torch.cuda.synchronize()
-            render_dev(cfg_s)
-            for key, v in r.stats()["stage_ms"].items():
-                stage_sum[key] = stage_sum.get(key, 0.0) + v
+            fn()
+            for key, v in self.r.stats()["stage_ms"].items():
+                acc[key] = acc.get(key, 0.0) + v
         torch.cuda.synchronize()
-        r.set_timing(False)
-        stages = {k: v / reps / frames_per_step for k, v in stage_sum.items()}
-        return ms, stages, launches, (sampler.summary() if sampler else None)
+        self.r.set_timing(False)
+        return {k: v / reps / views for k, v in acc.items()}
 
-    cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg)
+
+def run_ours(args) -> None:
+    import ctypes as C
+
+    import numpy as np
+
+    o = Ours(args)
+    torch, api, lib, r = o.torch, o.api, o.lib, o.r
+    world, rank = o.world, o.rank
+    kind, seed, n, w, h, nviews = WORKLOADS[args.workload]
+    splats = None
+    scene = api.Scene.synthetic(kind, seed, n)
+    deg = scene.sh_degree
+    cams = api.orbit_cameras(nviews, w, h)
+    # one view per rank per step (weak scaling); rank 0 renders orbit view 0
+    my_view = (rank * max(1, nviews // max(world, 1))) % nviews
+    cam = cams[my_view]
+    ds = r.upload(scene)
+    out_rgb = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+    out_t = torch.empty((h, w), dtype=torch.float32, device="cuda")
+    cfg = o.cfg(HEADLINE[1], HEADLINE[2], deg)
     cfg_s = cfg.to_struct()
-    ms, stages, launches, clocks = timed(cfg_s, args.steps, args.warmup, sample_clocks=True)
-    fps = world * frames_per_step * 1000.0 / ms
+    step = o.render_fn(ds, [cam.to_struct()], cfg_s, out_rgb, out_t)
 
-    # work counters of the timed frame (untimed render with counters)
-    fb_unused, ctr = r.render(ds, cam, cfg, counters=True)
+    ms, launches, clocks = o.timed(step, args.steps, args.warmup, sample_clocks=True)
+    fps = world * 1000.0 / ms
+    # the LAST timed step's image (still in out_rgb / out_t): parity below
+    timed_rgb, timed_t = out_rgb.cpu().numpy(), out_t.cpu().numpy()
+    stages = o.stage_split(step, max(3, min(args.steps, 20)))
+    # work counters of the same frame (the counting instantiation, untimed)
+    _, ctr = r.render(ds, cam, cfg, counters=True)
     st = r.stats()
     result = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
               "vs_baseline": None, "dtype": "f32 blend, f64 preprocess/binning", "data": "synthetic",
               "config": workload_config(args.workload), "gaussians_per_s": fps * n,
-              "gpu_launches": launches, "clocks": clocks}
-    result["config"]["views_per_rank_per_step"] = frames_per_step
+              "gpu_launches": launches, "gpu_launches_per_step": launches / max(args.steps, 1), "clocks": clocks,
+              "views_per_rank_per_step": 1, "gpus_active": world}
     result["stages_ms"] = stages
     result["work"] = {"visible": st["visible"], "pairs": st["pairs"], "kernel_evaluations": ctr.kernel_evaluations,
                       "fragments_blended": ctr.fragments_blended, "replay_pixels": st["replay_pixels"],
                       "exact_alpha_evals": st["exact_alpha_evals"]}
-
     if rank == 0:
-        rstages = stages
-        if batch:
-            # the batched step's per-view stage times overlap across the views'
-            # streams; the roofline uses single-view renders of the same workload
-            r.set_timing(True)
-            acc, reps = {}, 5
-            for _ in range(reps):
-                flush.zero_()
-                torch.cuda.synchronize()
-                st_ = lib.ps_render(r.handle, ds.handle, C.byref(cam_structs[0]), C.byref(cfg_s),
-                                    out_rgb.data_ptr(), out_t.data_ptr(), 1, None)
-                if st_ != 0:
-                    raise RuntimeError(api.last_error(r.handle))
-                for key, v in r.stats()["stage_ms"].items():
-                    acc[key] = acc.get(key, 0.0) + v / reps
-            r.set_timing(False)
-            rstages = acc
-            result["stages_ms_single_view"] = acc
-        result["roofline"], result["roofline_stages"] = roofline(r, rstages, n, deg, st, ctr, HEADLINE[1],
+        result["roofline"], result["roofline_stages"] = roofline(r, stages, n, deg, st, ctr, HEADLINE[1],
                                                                  args.workload)
-        if batch:
-            result["roofline"]["note"] = "stage times of single-view renders (batched views overlap across streams)"
 
-    # poly-vs-exp and the rest of the kernel matrix (fewer steps each)
+    # the reference's ablation cells with device times (f4), and image quality
+    # of every cell against exp / StopThePop (polysplat::compare, metrics.cpp:138-157)
     if not args.no_compare:
-        kern = {HEADLINE[0]: {"frames_per_s": fps / world, "ms": ms / frames_per_step, "pairs": st["pairs"]}}
-        for label, kname, mode in COMPARE:
-            c2 = make_cfg(api, kname, mode, deg).to_struct()
-            m2, _, _, _ = timed(c2, max(3, min(args.steps, 10)), 3)
-            kern[label] = {"frames_per_s": frames_per_step * 1000.0 / m2, "ms": m2 / frames_per_step,
-                           "pairs": r.stats()["pairs"] // frames_per_step}  # per view
-        # image quality of every kernel against exp / StopThePop (the paper's
-        # comparison point), on the device: polysplat::compare (metrics.cpp:138-157)
-        ref_cfg = make_cfg(api, "exp", "StopThePop", deg)
-        for label, kname, mode in [HEADLINE] + COMPARE:
-            if label == "exp/stp":
-                continue
-            rep = r.compare(ds, cam, ref_cfg, make_cfg(api, kname, mode, deg))
-            kern[label].update({"psnr_vs_exp_db": rep.psnr_db, "ssim_vs_exp": rep.ssim,
-                                "pair_ratio_vs_exp": rep.pair_ratio})
-        result["kernels"] = kern
-        result["poly1_vs_exp_speedup"] = kern["exp/stp"]["ms"] / kern[HEADLINE[0]]["ms"]
+        ref_cfg = o.cfg("exp", "StopThePop", deg)
+        abl = {}
+        for label, kname, mode in ABLATION:
+            c2 = o.cfg(kname, mode, deg)
+            fn = o.render_fn(ds, [cam.to_struct()], c2.to_struct(), out_rgb, out_t)
+            m2, _, _ = o.timed(fn, max(3, min(args.steps, 10)), 3)
+            sp = o.stage_split(fn, 3)
+            _, c_ = r.render(ds, cam, c2, counters=True)
+            cell = {"frames_per_s": 1000.0 / m2, "ms": m2, "blend_ms": sp.get("blend", 0.0),
+                    "preprocess_ms": sp.get("preprocess", 0.0), "pairs": c_.tile_pairs_after_tight_test,
+                    "kernel_evaluations": c_.kernel_evaluations, "fragments_blended": c_.fragments_blended}
+            if label != "exp/stp":
+                rep = r.compare(ds, cam, ref_cfg, c2)
+                cell.update({"psnr_vs_exp_db": rep.psnr_db, "ssim_vs_exp": rep.ssim,
+                             "pair_ratio_vs_exp": rep.pair_ratio})
+            abl[label] = cell
+        result["ablation"] = abl
+        result["poly1_vs_exp_speedup"] = abl["exp/stp"]["ms"] / abl[HEADLINE[0]]["ms"]
 
-    # end to end through the public API with host buffers: H2D of the scene
-    # from pinned memory + render + D2H of the image, every frame. Two host
-    # threads, each with its own context (CUDA stream) and scene copy, as the
-    # C ABI's threading model allows, so one frame's H2D overlaps the other's
-    # render and D2H (the PCIe H2D of the 280 MB scene is the bound).
+    # C5 culling ablation: universal (zero-crossing) vs opacity-aware bound on
+    # the skewed-opacity scene: key count and blend time (BASELINE.json config 5)
+    if not args.no_c5 and args.workload == "c2":
+        k5, s5, n5, w5, h5, _ = WORKLOADS["c5"]
+        sc5 = api.Scene.synthetic(k5, s5, n5)
+        ds5 = r.upload(sc5)
+        cam5 = api.orbit_cameras(256, w5, h5)[0]
+        c5 = {}
+        for label, kname, mode in [("poly1/zero", "poly1", "ZeroCrossing"), ("poly1/opacity", "poly1", "OpacityAware"),
+                                   ("exp/stp", "exp", "StopThePop")]:
+            cc = o.cfg(kname, mode, sc5.sh_degree)
+            fn = o.render_fn(ds5, [cam5.to_struct()], cc.to_struct(), out_rgb, out_t)
+            m5, _, _ = o.timed(fn, max(3, min(args.steps, 10)), 3)
+            sp = o.stage_split(fn, 3)
+            _, c_ = r.render(ds5, cam5, cc, counters=True)
+            c5[label] = {"ms": m5, "frames_per_s": 1000.0 / m5, "blend_ms": sp.get("blend", 0.0),
+                         "keys": c_.tile_pairs_after_tight_test, "visible": r.stats()["visible"],
+                         "fragments_blended": c_.fragments_blended, "kernel_evaluations": c_.kernel_evaluations}
+        c5["key_reduction"] = 1.0 - c5["poly1/opacity"]["keys"] / c5["poly1/zero"]["keys"]
+        c5["blend_speedup"] = c5["poly1/zero"]["blend_ms"] / max(c5["poly1/opacity"]["blend_ms"], 1e-9)
+        result["c5_culling_ablation"] = c5
+        ds5.close()
+        del sc5
+
+    # C4: the 256-view batch of a 3M scene sharded over the ranks (strong
+    # scaling; BASELINE.json config 4): every rank renders its contiguous shard
+    # through ps_render_views each step
+    if not args.no_c4 and args.workload == "c2":
+        from paper_2603_18707_b200.sharding import shard_views
+        k4, s4, n4, w4, h4, v4 = WORKLOADS["c4"]
+        sc4 = api.Scene.synthetic(k4, s4, n4)
+        ds4 = r.upload(sc4)
+        cams4 = api.orbit_cameras(v4, w4, h4)
+        mine = list(shard_views(v4, world, rank))
+        o4_rgb = torch.empty((len(mine), h4, w4, 3), dtype=torch.float32, device="cuda")
+        o4_t = torch.empty((len(mine), h4, w4), dtype=torch.float32, device="cuda")
+        fn = o.render_fn(ds4, [cams4[v].to_struct() for v in mine], o.cfg("poly1", "OpacityAware", sc4.sh_degree).to_struct(),
+                         o4_rgb, o4_t)
+        m4, l4, _ = o.timed(fn, max(2, min(args.steps, 3)), 1)
+        result["c4_sharded"] = {"views_per_s": v4 * 1000.0 / m4, "ms_per_batch": m4, "views": v4,
+                                "views_per_rank": len(mine), "gpus_active": world, "scaling": "strong",
+                                "gaussians_per_s": v4 * n4 * 1000.0 / m4, "gpu_launches_per_batch": l4 / max(2, min(args.steps, 3)),
+                                "kernel": "poly1/opacity", "path": "ps_render_views per rank, scene replicated, no collective"}
+        ds4.close()
+        del sc4, o4_rgb, o4_t
+
+    # end to end through the public API with host buffers
     if not args.no_e2e:
-        import threading
-        pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(scene, k))).pin_memory()
-               for k in ("means", "scales", "rotations", "opacities", "sh")}
-        r2 = api.Rasterizer(local)
-        ds2 = r2.upload(scene)
-        lanes = [(r, ds), (r2, ds2)]
-        streams = [stream, torch.cuda.ExternalStream(lib.ps_ctx_stream(r2.handle), device=torch.device("cuda", local))]
-        outs = [(torch.empty((h, w, 3), dtype=torch.float32).pin_memory(),
-                 torch.empty((h, w), dtype=torch.float32).pin_memory()) for _ in lanes]
-        ke = max(4, min(args.steps, 12))
-        errors = []
+        result["e2e"] = e2e_soa(o, scene, ds, [cam.to_struct()], cfg_s, w, h, args)
+        splats = api.synthetic_splat3d(_scene_key(kind), seed, n)[0]
+        result["e2e_dropin"] = e2e_dropin(o, splats, cam, cfg_s, args)
 
-        def e2e_frame(li):
-            rr, dd = lanes[li]
-            hr, ht = outs[li]
-            stt = lib.ps_scene_update_soa(rr.handle, dd.handle, pin["means"].data_ptr(), pin["scales"].data_ptr(),
-                                          pin["rotations"].data_ptr(), pin["opacities"].data_ptr(),
-                                          pin["sh"].data_ptr(), 0)
-            if stt != 0:
-                raise RuntimeError(api.last_error(rr.handle))
-            for cs in cam_structs:
-                stt = lib.ps_render(rr.handle, dd.handle, C.byref(cs), C.byref(cfg_s), hr.data_ptr(), ht.data_ptr(),
-                                    0, None)
-                if stt != 0:
-                    raise RuntimeError(api.last_error(rr.handle))
-
-        def worker(li, nframes):
-            try:
-                for _ in range(nframes):
-                    e2e_frame(li)
-            except Exception as ex:  # surfaced after join
-                errors.append(ex)
-
-        for li in range(len(lanes)):  # warm-up, untimed
-            e2e_frame(li)
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(streams[0])
-        streams[1].wait_event(e0)
-        per_lane = [ke // 2 + (ke % 2 if li == 0 else 0) for li in range(len(lanes))]
-        ths = [threading.Thread(target=worker, args=(li, per_lane[li])) for li in range(len(lanes))]
-        for t_ in ths:
-            t_.start()
-        for t_ in ths:
-            t_.join()
-        if errors:
-            raise errors[0]
-        ends = []
-        for s_ in streams:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(s_)
-            ends.append(ev)
-        torch.cuda.synchronize()
-        ems = max(e0.elapsed_time(ev) for ev in ends) / ke
-        if dist:
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        ds2.close()
-        r2.close()
-        h2d = sum(v.numel() * v.element_size() for v in pin.values())
-        result["e2e"] = {"value": world * frames_per_step * 1000.0 / ems, "unit": "frames/s", "ms_per_step": ems,
-                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(frames_per_step * h * w * 16),
-                         "frames_timed": ke,
-                         "path": "per frame: ps_scene_update_soa (pinned host SoA) + ps_render (host outputs); "
-                                 "2 host threads x 2 contexts, device-timed over all frames"}
-
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args.workload, (fb_unused, ctr))
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args.workload, (timed_rgb, timed_t, ctr), world)
 
     ds.close()
     r.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    if o.dist:
+        o.dist.barrier()
+        o.dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
 
 
+def e2e_soa(o, scene, ds, cam_structs, cfg_s, w, h, args) -> dict:
+    """Per frame: ps_scene_update_soa from pinned host SoA + ps_render into pinned
+    host outputs. Two host threads, each with its own context (CUDA stream) and
+    scene copy, as the C ABI's threading model allows, so one frame's H2D
+    overlaps the other's render and D2H (the PCIe H2D of the 280 MB scene is the
+    bound). Device-timed over all frames."""
+    import ctypes as C
+    import threading
+
+    import numpy as np
+    torch, api, lib, r = o.torch, o.api, o.lib, o.r
+    pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(scene, k))).pin_memory()
+           for k in ("means", "scales", "rotations", "opacities", "sh")}
+    r2 = api.Rasterizer(o.local)
+    ds2 = r2.upload(scene)
+    lanes = [(r, ds), (r2, ds2)]
+    streams = [o.stream, torch.cuda.ExternalStream(lib.ps_ctx_stream(r2.handle), device=torch.device("cuda", o.local))]
+    outs = [(torch.empty((h, w, 3), dtype=torch.float32).pin_memory(),
+             torch.empty((h, w), dtype=torch.float32).pin_memory()) for _ in lanes]
+    ke = max(4, min(args.steps, 12))
+    errors = []
+
+    def frame(li):
+        rr, dd = lanes[li]
+        hr, ht = outs[li]
+        stt = lib.ps_scene_update_soa(rr.handle, dd.handle, pin["means"].data_ptr(), pin["scales"].data_ptr(),
+                                      pin["rotations"].data_ptr(), pin["opacities"].data_ptr(),
+                                      pin["sh"].data_ptr(), 0)
+        if stt != 0:
+            raise RuntimeError(api.last_error(rr.handle))
+        for cs in cam_structs:
+            stt = lib.ps_render(rr.handle, dd.handle, C.byref(cs), C.byref(cfg_s), hr.data_ptr(), ht.data_ptr(),
+                                0, None)
+            if stt != 0:
+                raise RuntimeError(api.last_error(rr.handle))
+
+    def worker(li, nframes):
+        try:
+            for _ in range(nframes):
+                frame(li)
+        except Exception as ex:  # surfaced after join
+            errors.append(ex)
+
+    for li in range(len(lanes)):  # warm-up, untimed
+        frame(li)
+    o.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(streams[0])
+    streams[1].wait_event(e0)
+    per_lane = [ke // 2 + (ke % 2 if li == 0 else 0) for li in range(len(lanes))]
+    ths = [threading.Thread(target=worker, args=(li, per_lane[li])) for li in range(len(lanes))]
+    for t_ in ths:
+        t_.start()
+    for t_ in ths:
+        t_.join()
+    if errors:
+        raise errors[0]
+    ends = []
+    for s_ in streams:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(s_)
+        ends.append(ev)
+    torch.cuda.synchronize()
+    ems = o.max_ms(max(e0.elapsed_time(ev) for ev in ends) / ke)
+    ds2.close()
+    r2.close()
+    h2d = sum(v.numel() * v.element_size() for v in pin.values())
+    return {"value": o.world * 1000.0 / ems, "unit": "frames/s", "ms_per_step": ems,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h * w * 16), "frames_timed": ke,
+            "path": "per frame: ps_scene_update_soa (pinned host SoA) + ps_render (host outputs); "
+                    "2 host threads x 2 contexts, device-timed over all frames"}
+
+
+def e2e_dropin(o, splats, cam, cfg_s, args) -> dict:
+    """The literal drop-in: ps_render_splats (polysplat::b200::render(span<Splat3D>))
+    with the reference's host Splat3D array (pageable, 472 B per splat) in and
+    an fp64 host framebuffer out, every frame; synchronous call, host wall time."""
+    import ctypes as C
+
+    import numpy as np
+    api, lib, r = o.api, o.lib, o.r
+    a = np.ascontiguousarray(splats, dtype=np.float64)
+    cs = cam.to_struct()
+    rgb = np.zeros((cam.height, cam.width, 3))
+    tr = np.zeros((cam.height, cam.width))
+    dp = C.POINTER(C.c_double)
+
+    def call():
+        st = lib.ps_render_splats(r.handle, a.ctypes.data_as(dp), len(a), C.byref(cs), C.byref(cfg_s),
+                                  rgb.ctypes.data_as(dp), tr.ctypes.data_as(dp), None)
+        if st != 0:
+            raise RuntimeError(api.last_error(r.handle))
+
+    for _ in range(2):
+        call()
+    ke = max(3, min(args.steps, 8))
+    o.barrier()
+    times = []
+    for _ in range(ke):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    ms = o.max_ms(1000.0 * statistics.median(times))
+    pix = cam.width * cam.height
+    h2d = len(a) * 280  # the compact upload record (fp64 geometry + fp32 SH) the host workers write
+    d2h = pix * 16 + o.r.stats()["replay_pixels"] * 36
+    io_ref = a.nbytes + pix * 32  # the reference interface's bytes: Splat3D array in, fp64 framebuffer out
+    return {"value": o.world * 1000.0 / ms, "unit": "frames/s", "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "frames_timed": ke,
+            "interface_bytes_per_step": int(io_ref),
+            "pcie_ms_of_interface_bytes_at_53GBps": io_ref / 53e9 * 1e3,
+            "vs_pcie_time_of_interface_bytes": ms / (io_ref / 53e9 * 1e3),
+            "path": "ps_render_splats: pageable host Splat3D array (472 B/splat) -> host threads narrow it to "
+                    "280-B records in a pinned chunk ring -> DMA -> device split + Morton upload -> render -> "
+                    "fp32 image + exact replay values -> fp64 host framebuffer; median host wall time of "
+                    "synchronous calls"}
+
+
 def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workload: str = "c2"):
-    """Per-stage achieved vs peak; the dominant stage goes to the top-level `roofline`."""
+    """Per-stage achieved vs peak; the dominant stage goes to the top-level `roofline`.
+    The blend's time includes its per-tile bucket sort (prologue) and the fused
+    exact replay; the tile sort has no separate stage of its own."""
     import ctypes as C
 
     from paper_2603_18707_b200 import api
@@ -420,7 +559,6 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workl
     work = {  # SURVEY §8(d) algorithmic work per stage
         "preprocess": ("hbm", n * (88 + sh_bytes) + v * 64),
         "duplicate": ("hbm", p * 12),
-        "tile_sort": ("hbm", p * 12 * 2),
         "blend": ("fp32", OPS_PER_EVAL.get(kname, 8) * E + OPS_PER_BLEND * B),
     }
     out = {}
@@ -438,6 +576,8 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workl
             out[name] = {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "Tinst/s", "frac": ach / peak,
                          "algorithmic": amount, "ms": ms,
                          "peak_source": f"measured FFMA microbenchmark {fp32_tflops:.1f} TFLOP/s"}
+    if "blend" in out:
+        out["blend"]["includes"] = "per-tile (depth, index) bucket sort in the prologue + fused fp64 replay"
     dom = max(out, key=lambda k: out[k]["ms"]) if out else None
     top = dict(out[dom]) if dom else {}
     if dom:
@@ -452,7 +592,7 @@ def roofline(r, stages: dict, n: int, deg: int, st: dict, ctr, kname: str, workl
 
 
 # stage -> kernel-name prefix in the ncu captures (blend: the 16x16 kernel of the headline kernel class)
-_STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0", "preprocess": "k_preprocess<3, 1, 3>", "duplicate": "k_duplicate_buckets"}
+_STAGE_KERNEL = {"blend": "k_blend16<1, 1, 0, 0", "preprocess": "k_preprocess<3, 1, 3>", "duplicate": "k_duplicate_buckets"}
 
 
 def profiled_traffic(stage: str, kname: str, workload: str = "c2"):
@@ -480,23 +620,25 @@ def profiled_traffic(stage: str, kname: str, workload: str = "c2"):
 
 
 def full_size_parity(ours, ref_out) -> dict:
-    """Our timed frame vs the reference's image of the same frame: max-abs per
-    channel and transmittance, PSNR of the white-background composite
-    (metrics.cpp:13-44), and the six work counters."""
+    """The last timed step's image vs the reference's image of the same frame:
+    max-abs per channel and transmittance, PSNR of the white-background
+    composite (metrics.cpp:13-44), and the six work counters (of the counting
+    render of the same frame)."""
     import numpy as np
-    fb, ctr = ours
+    rgb_o, t_o, ctr = ours
     rgb, tr, ctr_ref = ref_out
-    d_rgb = float(np.max(np.abs(fb.rgb.astype(np.float64) - rgb)))
-    d_t = float(np.max(np.abs(fb.transmittance.astype(np.float64) - tr)))
-    ca = fb.rgb.astype(np.float64) + fb.transmittance.astype(np.float64)[..., None]
+    d_rgb = float(np.max(np.abs(rgb_o.astype(np.float64) - rgb)))
+    d_t = float(np.max(np.abs(t_o.astype(np.float64) - tr)))
+    ca = rgb_o.astype(np.float64) + t_o.astype(np.float64)[..., None]
     cb = rgb + tr[..., None]
     mse = float(np.mean((ca - cb) ** 2))
-    return {"max_abs_rgb": d_rgb, "max_abs_t": d_t, "tolerance": 1e-5,
+    return {"frame": "last timed step (counter-free blend, device outputs)", "max_abs_rgb": d_rgb, "max_abs_t": d_t,
+            "tolerance": 1e-5, "within_tolerance": d_rgb <= 1e-5 and d_t <= 1e-5,
             "psnr_db": None if mse == 0.0 else 10.0 * float(np.log10(1.0 / mse)),
             "counters_identical": ctr.as_dict() == ctr_ref}
 
 
-def cpu_baseline(workload: str, ours=None) -> dict:
+def cpu_baseline(workload: str, ours=None, world: int = 1) -> dict:
     """The reference's own renderer (oracle/_ref) on this host, bounded sample;
     its image of the frame also checks our timed frame at full size."""
     try:
@@ -504,10 +646,15 @@ def cpu_baseline(workload: str, ours=None) -> dict:
         from paper_2603_18707_b200 import api
         kind, seed, n, w, h, _ = WORKLOADS[workload]
         ref = oracle.Reference()
-        splats, deg = api.synthetic_splat3d({"g": 3, "skewed": 4}[kind], seed, n)
-        cam = api.orbit_cameras(256, w, h)[0].to_struct()
-        cfg = make_cfg(api, HEADLINE[1], HEADLINE[2], deg).to_struct()
+        splats, deg = ref.synth_g(n, seed, kind == "skewed")
+        cam = ref.orbit_cameras(256, w, h)[0]
+        cfg = api.RasterConfig(kernel=api.fitted_kernel(HEADLINE[1]),
+                               culling_mode=getattr(api.CullingMode, HEADLINE[2]), sh_degree=deg).to_struct()
         ref_out = ref.render(splats, cam, cfg)  # warm-up (its image is the parity check)
+        parity = full_size_parity(ours, ref_out) if ours is not None else None
+        if world > 1:
+            return {"parity": parity, "value": None, "unit": "frames/s", "kind": "reference",
+                    "sample": "not timed at N > 1 (rank 0 parity only)"}
         ts = []
         for _ in range(3):
             t0 = time.perf_counter()
@@ -522,8 +669,8 @@ def cpu_baseline(workload: str, ours=None) -> dict:
             ref.count_pairs(splats, cam, cfg)
             tc.append(time.perf_counter() - t0)
         mc = 1000.0 * statistics.median(tc)
-        parity = full_size_parity(ours, ref_out) if ours is not None else None
-        return {"parity": parity, "value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0), "kind": "reference",
+        return {"parity": parity, "value": 1000.0 / ms, "unit": "frames/s", "cores": ref.resolve_thread_count(0),
+                "cpu_model": cpu_model(), "kind": "reference",
                 "ms_per_frame": ms, "stage_split_ms": {"prepare_and_bin": mc, "blend": ms - mc},
                 "sample": f"median of 3 full {workload.upper()} frames ({HEADLINE[0]}), "
                           "polysplat::render built from the reference sources, all host threads"}
@@ -540,6 +687,8 @@ def main() -> None:
     ap.add_argument("--workload", choices=list(WORKLOADS), default="c2")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -6,10 +6,17 @@
 // One host sync per frame (after the count scan, to size the pair buffers and
 // surface device-side errors), plus the final copy-out.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -38,6 +45,100 @@ void host_camera_position(const ps_camera& cam, double out[3]);
 } // namespace ps
 
 using namespace ps;
+
+namespace {
+
+// Persistent host worker threads for the drop-in path's host-side passes
+// (copying the caller's Splat3D array into pinned chunks, widening the fp32
+// image into the caller's fp64 framebuffer). run() shares ntasks among the
+// workers and the calling thread and returns when all are done.
+class HostPool {
+public:
+    explicit HostPool(int n) : n_(std::max(n, 1)) {
+        for (int i = 1; i < n_; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    int size() const { return n_; }
+    void run(int ntasks, const std::function<void(int)>& fn) {
+        if (n_ == 1 || ntasks <= 1) {
+            for (int k = 0; k < ntasks; ++k) fn(k);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> g(m_);
+            fn_ = &fn;
+            ntasks_ = ntasks;
+            next_.store(0);
+            pending_ = n_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> g(m_);
+        done_.wait(g, [&] { return pending_ == 0; });
+    }
+
+private:
+    void work() {
+        for (int k; (k = next_.fetch_add(1)) < ntasks_;) (*fn_)(k);
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            work();
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int ntasks_ = 0;
+    std::atomic<int> next_{0};
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+int host_threads() {
+    if (const char* e = std::getenv("PS_HOST_THREADS")) {
+        const int v = std::atoi(e);
+        if (v > 0) return std::min(v, 64);
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    return static_cast<int>(std::min(std::max(hc, 1u), 32u));
+}
+
+// PS_TRACE_DROPIN=1: phase times of the drop-in path on stderr (diagnostic)
+bool trace_dropin() {
+    static const bool on = std::getenv("PS_TRACE_DROPIN") != nullptr;
+    return on;
+}
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// pinned upload ring of the drop-in path: kRing chunks of kChunk bytes
+constexpr int kRing = 4;
+constexpr size_t kChunk = size_t(16) << 20;
+
+} // namespace
 
 struct ps_scene {
     ps_ctx* ctx = nullptr;
@@ -86,6 +187,18 @@ struct ps_ctx {
     // with its own frame arrays, counters and stream
     std::vector<ps_ctx*> views;
     cudaEvent_t k1_event = nullptr;
+    // drop-in path (ps_render_splats, ps_scene_create_aos): a reusable scene,
+    // the raw Splat3D array on the device, a pinned chunk ring (AoS upload),
+    // pinned image readback, host worker threads
+    ps_scene* dropin = nullptr;
+    int64_t dropin_cap = 0;
+    void* aos_dev = nullptr;
+    size_t aos_dev_bytes = 0;
+    char* ring = nullptr;
+    cudaEvent_t ring_ev[kRing] = {};
+    void* pin_out = nullptr;
+    size_t pin_out_bytes = 0;
+    std::unique_ptr<HostPool> pool;
 };
 
 namespace {
@@ -632,14 +745,18 @@ int render_one(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_conf
     return PS_OK;
 }
 
-int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales, const double* rots,
-               const double* opac, const float* sh, int memspace) {
-    const int64_t n = s->n;
-    if (n == 0) return PS_OK;
-    const cudaMemcpyKind kind = memspace == PS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // Stage the raw arrays (a few large DMAs; full link rate when the host
-    // buffers are pinned), order the splats along a Morton curve of their means,
-    // and gather them into the scene's SoA planes in that order.
+// Device staging of one scene upload: the raw arrays (fp64 geometry interleaved
+// per splat: means | scales | rots | opacity; SH as n x 48 fp32) and the Morton
+// sort's keys / scratch.
+struct Staging {
+    double* st = nullptr;
+    float4* sh_st = nullptr;
+    uint32_t* keys = nullptr;
+    unsigned long long* bb = nullptr;
+    void* scratch = nullptr;
+};
+
+int stage_alloc(ps_ctx* c, int64_t n, Staging& S) {
     // (every region 256-byte aligned: an odd n leaves 88 n bytes of fp64
     // geometry, which would misalign the float4 SH staging after it)
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
@@ -656,35 +773,149 @@ int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales
         c->stage_bytes = stage_bytes;
     }
     char* p = static_cast<char*>(c->stage);
-    double* st = reinterpret_cast<double*>(p);                       // means | scales | rots | opacity
-    float4* sh_st = reinterpret_cast<float4*>(p + geo);
-    uint32_t* keys = reinterpret_cast<uint32_t*>(p + geo + shb);
-    uint32_t* keys_alt = keys + n;
-    uint32_t* vals = keys + 2 * n;
-    uint32_t* vals_alt = keys + 3 * n;
-    unsigned long long* bb = reinterpret_cast<unsigned long long*>(p + geo + shb + keyb);
-    void* scratch = reinterpret_cast<char*>(bb) + 256;
-    CTX_TRY(c, cudaMemcpyAsync(st, means, sizeof(double) * 3 * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
-    CTX_TRY(c, cudaMemcpyAsync(st + 10 * n, opac, sizeof(double) * n, kind, c->stream));
-    // exactly the caller's 48 n floats (shb only pads the staging layout)
-    CTX_TRY(c, cudaMemcpyAsync(sh_st, sh, sizeof(float) * 48 * static_cast<size_t>(n), kind, c->stream));
-    launch_morton_order(st, n, bb, keys, vals, c->stream);
-    const bool alt = radix_sort_u32(keys, keys_alt, vals, vals_alt, nullptr, n, 0, 30, scratch, c->stream, nullptr);
-    launch_gather_scene(st, st + 10 * n, sh_st, alt ? vals_alt : vals, n, s->dev, c->stream);
+    S.st = reinterpret_cast<double*>(p);
+    S.sh_st = reinterpret_cast<float4*>(p + geo);
+    S.keys = reinterpret_cast<uint32_t*>(p + geo + shb);
+    S.bb = reinterpret_cast<unsigned long long*>(p + geo + shb + keyb);
+    S.scratch = reinterpret_cast<char*>(S.bb) + 256;
+    return PS_OK;
+}
+
+// Orders the staged splats along a Morton curve of their means and gathers
+// them into the scene's SoA planes in that order (+ the 3D covariances).
+int finish_upload(ps_ctx* c, ps_scene* s, const Staging& S) {
+    const int64_t n = s->n;
+    uint32_t* keys_alt = S.keys + n;
+    uint32_t* vals = S.keys + 2 * n;
+    uint32_t* vals_alt = S.keys + 3 * n;
+    launch_morton_order(S.st, n, S.bb, S.keys, vals, c->stream);
+    const bool alt = radix_sort_u32(S.keys, keys_alt, vals, vals_alt, nullptr, n, 0, 30, S.scratch, c->stream, nullptr);
+    launch_gather_scene(S.st, S.st + 10 * n, S.sh_st, alt ? vals_alt : vals, n, s->dev, c->stream);
     launch_scene_cov(s->dev, c->stream);
     CTX_TRY(c, cudaStreamSynchronize(c->stream));
     CTX_TRY(c, cudaGetLastError());
     return PS_OK;
 }
 
-int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out) {
+int upload_soa(ps_ctx* c, ps_scene* s, const double* means, const double* scales, const double* rots,
+               const double* opac, const float* sh, int memspace) {
+    const int64_t n = s->n;
+    if (n == 0) return PS_OK;
+    const cudaMemcpyKind kind = memspace == PS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // Stage the raw arrays (a few large DMAs; full link rate when the host
+    // buffers are pinned), then order and gather them on the device.
+    Staging S;
+    int st = stage_alloc(c, n, S);
+    if (st != PS_OK) return st;
+    CTX_TRY(c, cudaMemcpyAsync(S.st, means, sizeof(double) * 3 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(S.st + 3 * n, scales, sizeof(double) * 3 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(S.st + 6 * n, rots, sizeof(double) * 4 * n, kind, c->stream));
+    CTX_TRY(c, cudaMemcpyAsync(S.st + 10 * n, opac, sizeof(double) * n, kind, c->stream));
+    // exactly the caller's 48 n floats (the staging layout only pads the region)
+    CTX_TRY(c, cudaMemcpyAsync(S.sh_st, sh, sizeof(float) * 48 * static_cast<size_t>(n), kind, c->stream));
+    return finish_upload(c, s, S);
+}
+
+HostPool& pool_of(ps_ctx* c) {
+    if (!c->pool) c->pool = std::make_unique<HostPool>(host_threads());
+    return *c->pool;
+}
+
+// Host (pageable) -> device transfer through the context's pinned chunk ring:
+// the host workers fill chunk k of a free ring slot while the DMA engine moves
+// chunk k-1 (a pageable cudaMemcpy would bounce through the driver's small
+// staging buffers at a fraction of the link rate). fill(dst, first, count)
+// writes `count` records starting at record `first` (rec_bytes each) into
+// pinned memory.
+int h2d_chunked(ps_ctx* c, void* dst, int64_t records, size_t rec_bytes,
+                const std::function<void(char*, int64_t, int64_t)>& fill) {
+    if (records == 0) return PS_OK;
+    if (!c->ring) {
+        CTX_TRY(c, cudaMallocHost(reinterpret_cast<void**>(&c->ring), kRing * kChunk));
+        for (auto& e : c->ring_ev) CTX_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    HostPool& pool = pool_of(c);
+    char* d = static_cast<char*>(dst);
+    const int64_t per_chunk = static_cast<int64_t>(kChunk / rec_bytes);
+    double t_wait = 0.0, t_copy = 0.0;
+    const bool tr = trace_dropin();
+    int64_t first = 0;
+    for (int k = 0; first < records; ++k) {
+        const int slot = k % kRing;
+        const double t0 = tr ? now_ms() : 0.0;
+        if (k >= kRing) CTX_TRY(c, cudaEventSynchronize(c->ring_ev[slot]));
+        const double t1 = tr ? now_ms() : 0.0;
+        const int64_t cnt = std::min(per_chunk, records - first);
+        char* pin = c->ring + static_cast<size_t>(slot) * kChunk;
+        const int parts = cnt * rec_bytes >= (size_t(1) << 20) ? pool.size() : 1;
+        pool.run(parts, [&](int q) {
+            const int64_t a = cnt * q / parts, b = cnt * (q + 1) / parts;
+            fill(pin + a * rec_bytes, first + a, b - a);
+        });
+        if (tr) { t_wait += t1 - t0; t_copy += now_ms() - t1; }
+        CTX_TRY(c, cudaMemcpyAsync(d + first * rec_bytes, pin, cnt * rec_bytes, cudaMemcpyHostToDevice, c->stream));
+        CTX_TRY(c, cudaEventRecord(c->ring_ev[slot], c->stream));
+        first += cnt;
+    }
+    if (tr)
+        std::fprintf(stderr, "[dropin] h2d %lld x %zu B: host fill %.3f ms, ring waits %.3f ms (%d threads)\n",
+                     static_cast<long long>(records), rec_bytes, t_copy, t_wait, pool.size());
+    return PS_OK;
+}
+
+// Reference Splat3D array (host) -> scene. The host workers narrow each 472-B
+// record to the 280-B upload record (fp64 mean, scale, rotation, opacity; SH
+// rounded to fp32 — the scene keeps fp32 SH either way) while filling the
+// pinned ring, so both the host memory traffic and the PCIe bytes shrink by
+// 40%; the device splits the records into the staging layout. PS_DROPIN_RAW=1
+// ships the raw 472-B records instead (A/B).
+constexpr size_t kCompactRec = 11 * sizeof(double) + 48 * sizeof(float);
+
+int upload_aos(ps_ctx* c, ps_scene* s, const double* splats) {
+    const int64_t n = s->n;
+    if (n == 0) return PS_OK;
+    Staging S;
+    int st = stage_alloc(c, n, S);
+    if (st != PS_OK) return st;
+    static const bool raw = std::getenv("PS_DROPIN_RAW") != nullptr;
+    const size_t rec = raw ? sizeof(double) * PS_SPLAT3D_DOUBLES : kCompactRec;
+    const size_t bytes = rec * static_cast<size_t>(n);
+    if (bytes > c->aos_dev_bytes) {
+        if (c->aos_dev) cudaFree(c->aos_dev);
+        c->aos_dev = nullptr;
+        c->aos_dev_bytes = 0;
+        CTX_TRY(c, cudaMalloc(&c->aos_dev, bytes));
+        c->aos_dev_bytes = bytes;
+    }
+    if (raw) {
+        st = h2d_chunked(c, c->aos_dev, n, rec, [&](char* dst, int64_t first, int64_t cnt) {
+            std::memcpy(dst, splats + first * PS_SPLAT3D_DOUBLES, cnt * rec);
+        });
+    } else {
+        st = h2d_chunked(c, c->aos_dev, n, rec, [&](char* dst, int64_t first, int64_t cnt) {
+            for (int64_t i = 0; i < cnt; ++i) {
+                const double* sp = splats + (first + i) * PS_SPLAT3D_DOUBLES;
+                char* o = dst + i * kCompactRec;
+                std::memcpy(o, sp, 11 * sizeof(double));
+                float* f = reinterpret_cast<float*>(o + 11 * sizeof(double));
+                for (int k = 0; k < 48; ++k) f[k] = static_cast<float>(sp[11 + k]);
+            }
+        });
+    }
+    if (st != PS_OK) return st;
+    launch_split_records(static_cast<const double*>(c->aos_dev), n, raw, S.st, reinterpret_cast<float*>(S.sh_st),
+                         c->stream);
+    return finish_upload(c, s, S);
+}
+
+int alloc_scene(ps_ctx* c, int64_t n, ps_scene** out, int64_t capacity = 0) {
     auto* s = new ps_scene();
     s->ctx = c;
     s->n = n;
     s->dev.n = n;
-    const int64_t cap = std::max<int64_t>(n, 1);
+    // planes sized for `capacity` splats: a smaller scene reuses them (the SH
+    // planes are strided by the scene's own n, which only shrinks the region)
+    const int64_t cap = std::max<int64_t>(std::max(n, capacity), 1);
     const size_t plane = (sizeof(double) * cap + 255) & ~size_t(255);
     const size_t shb = (sizeof(float) * 48 * cap + 255) & ~size_t(255);
     const size_t origb = (sizeof(uint32_t) * cap + 255) & ~size_t(255);
@@ -762,6 +993,14 @@ void ps_ctx_destroy(ps_ctx* c) {
     for (ps_ctx* v : c->views) ps_ctx_destroy(v);
     c->views.clear();
     cudaSetDevice(c->device);
+    if (c->dropin) ps_scene_destroy(c->dropin);
+    c->dropin = nullptr;
+    c->pool.reset();
+    if (c->ring) cudaFreeHost(c->ring);
+    if (c->pin_out) cudaFreeHost(c->pin_out);
+    for (auto& e : c->ring_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->aos_dev) cudaFree(c->aos_dev);
     if (c->k1_event) cudaEventDestroy(c->k1_event);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& ev : c->ev)
@@ -842,19 +1081,17 @@ int ps_scene_update_soa(ps_ctx* c, ps_scene* s, const double* means, const doubl
 
 int ps_scene_create_aos(ps_ctx* c, const double* splats, int64_t n, ps_scene** out) {
     if (!c || !out || n < 0 || (n > 0 && !splats)) return set_err(c, PS_INVALID_ARGUMENT, "bad scene arguments");
-    const int64_t cap = std::max<int64_t>(n, 1);
-    std::vector<double> means(3 * cap), scales(3 * cap), rots(4 * cap), opac(cap);
-    std::vector<float> sh(48 * cap);
-    for (int64_t i = 0; i < n; ++i) {
-        const double* sp = splats + i * PS_SPLAT3D_DOUBLES;
-        for (int k = 0; k < 3; ++k) means[3 * i + k] = sp[k];
-        for (int k = 0; k < 3; ++k) scales[3 * i + k] = sp[3 + k];
-        for (int k = 0; k < 4; ++k) rots[4 * i + k] = sp[6 + k];
-        opac[i] = sp[10];
-        for (int k = 0; k < 48; ++k) sh[48 * i + k] = static_cast<float>(sp[11 + k]);
+    if (n > 0xFFFFFFFFll) return set_err(c, PS_INVALID_ARGUMENT, "scene too large (> 2^32 splats)");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    ps_scene* s = nullptr;
+    int st = alloc_scene(c, n, &s);
+    if (st != PS_OK) return st;
+    if ((st = upload_aos(c, s, splats)) != PS_OK) {
+        ps_scene_destroy(s);
+        return st;
     }
-    return ps_scene_create_soa(c, means.data(), scales.data(), rots.data(), opac.data(), sh.data(), n,
-                               PS_MEM_HOST, out);
+    *out = s;
+    return PS_OK;
 }
 
 int64_t ps_scene_size(const ps_scene* s) { return s ? s->n : -1; }
@@ -1025,35 +1262,80 @@ int ps_render_views(ps_ctx* c, const ps_scene* s, const ps_camera* cams, int n_v
 
 int ps_render_splats(ps_ctx* c, const double* splats, int64_t n, const ps_camera* cam, const ps_config* cfg,
                      double* out_rgb, double* out_t, ps_counters* counters) {
-    if (!c || !cam || !cfg) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    if (!c || !cam || !cfg || n < 0 || (n > 0 && !splats)) return set_err(c, PS_INVALID_ARGUMENT, "null argument");
+    if (n > 0xFFFFFFFFll) return set_err(c, PS_INVALID_ARGUMENT, "scene too large (> 2^32 splats)");
     int st = host_validate_config(*cfg);
     if (st != PS_OK) return set_err(c, st, "RasterConfig::validate: invalid configuration");
     st = host_validate_camera(*cam);
-    if (st != PS_OK) return set_err(c, st, "Camera::validate: invalid camera");
-    ps_scene* s = nullptr;
-    if ((st = ps_scene_create_aos(c, splats, n, &s)) != PS_OK) return st;
-    const int64_t pix = static_cast<int64_t>(cam->width) * cam->height;
-    std::vector<float> rgb(3 * pix), tr(pix);
-    FrameResult r;
-    st = render_one(c, s, cam, cfg, rgb.data(), tr.data(), PS_MEM_HOST, counters, true, &r);
-    if (st == PS_OK) {
-        for (int64_t k = 0; k < 3 * pix; ++k) if (out_rgb) out_rgb[k] = rgb[k];
-        for (int64_t k = 0; k < pix; ++k) if (out_t) out_t[k] = tr[k];
-        const unsigned long long nf = r.ctr.replay_px;
-        if (nf) {
-            std::vector<uint32_t> ids(nf);
-            std::vector<double4> vals(nf);
-            cudaMemcpy(ids.data(), c->f.flags, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost);
-            cudaMemcpy(vals.data(), c->replay_vals, sizeof(double4) * nf, cudaMemcpyDeviceToHost);
-            for (unsigned long long k = 0; k < nf; ++k) {
-                const uint32_t p = ids[k];
-                if (out_rgb) { out_rgb[3 * p] = vals[k].x; out_rgb[3 * p + 1] = vals[k].y; out_rgb[3 * p + 2] = vals[k].z; }
-                if (out_t) out_t[p] = vals[k].w;
-            }
-        }
+    if (st != PS_OK)
+        return set_err(c, st, st == PS_NON_ORTHONORMAL_ROTATION ? "camera rotation is not orthonormal"
+                                                                 : "Camera::validate: invalid camera");
+    CTX_TRY(c, cudaSetDevice(c->device));
+    // the context's drop-in scene, reallocated only when a call brings more splats
+    if (!c->dropin || c->dropin_cap < n) {
+        if (c->dropin) ps_scene_destroy(c->dropin);
+        c->dropin = nullptr;
+        c->dropin_cap = 0;
+        if ((st = alloc_scene(c, n, &c->dropin)) != PS_OK) return st;
+        c->dropin_cap = n;
     }
-    ps_scene_destroy(s);
-    return st;
+    ps_scene* s = c->dropin;
+    s->n = n;
+    s->dev.n = n;
+    const bool tr = trace_dropin();
+    const double t0 = tr ? now_ms() : 0.0;
+    if ((st = upload_aos(c, s, splats)) != PS_OK) return st;
+    const double t1 = tr ? now_ms() : 0.0;
+    FrameResult r;
+    if ((st = render_one(c, s, cam, cfg, nullptr, nullptr, PS_MEM_DEVICE, counters, true, &r)) != PS_OK) return st;
+    const double t2 = tr ? now_ms() : 0.0;
+    // read back the fp32 image and the exact fp64 values of the replayed
+    // pixels into pinned memory, then widen into the caller's fp64 framebuffer
+    // on the host workers and patch the replayed pixels
+    const int64_t pix = static_cast<int64_t>(cam->width) * cam->height;
+    const uint64_t nf = r.ctr.replay_px;
+    const size_t img_b = (sizeof(float) * 4 * static_cast<size_t>(pix) + 255) & ~size_t(255);
+    const size_t ids_b = (sizeof(uint32_t) * nf + 255) & ~size_t(255);
+    const size_t need = img_b + ids_b + sizeof(double4) * nf;
+    if (need > c->pin_out_bytes) {
+        if (c->pin_out) cudaFreeHost(c->pin_out);
+        c->pin_out = nullptr;
+        c->pin_out_bytes = 0;
+        CTX_TRY(c, cudaMallocHost(&c->pin_out, need + need / 8));
+        c->pin_out_bytes = need + need / 8;
+    }
+    float* h_rgb = static_cast<float*>(c->pin_out);
+    float* h_t = h_rgb + 3 * pix;
+    uint32_t* h_ids = reinterpret_cast<uint32_t*>(static_cast<char*>(c->pin_out) + img_b);
+    double4* h_vals = reinterpret_cast<double4*>(static_cast<char*>(c->pin_out) + img_b + ids_b);
+    if (pix > 0) {
+        if (out_rgb) CTX_TRY(c, cudaMemcpyAsync(h_rgb, c->img_rgb, sizeof(float) * 3 * pix, cudaMemcpyDeviceToHost, c->stream));
+        if (out_t) CTX_TRY(c, cudaMemcpyAsync(h_t, c->img_t, sizeof(float) * pix, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (nf) {
+        CTX_TRY(c, cudaMemcpyAsync(h_ids, c->f.flags, sizeof(uint32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
+        CTX_TRY(c, cudaMemcpyAsync(h_vals, c->replay_vals, sizeof(double4) * nf, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CTX_TRY(c, cudaStreamSynchronize(c->stream));
+    const double t3 = tr ? now_ms() : 0.0;
+    HostPool& pool = pool_of(c);
+    const int parts = pix >= (1 << 16) ? pool.size() : 1;
+    pool.run(parts, [&](int q) {
+        const int64_t a = pix * q / parts, b = pix * (q + 1) / parts;
+        if (out_rgb)
+            for (int64_t k = 3 * a; k < 3 * b; ++k) out_rgb[k] = h_rgb[k];
+        if (out_t)
+            for (int64_t k = a; k < b; ++k) out_t[k] = h_t[k];
+    });
+    for (uint64_t k = 0; k < nf; ++k) {
+        const uint32_t p = h_ids[k];
+        if (out_rgb) { out_rgb[3 * p] = h_vals[k].x; out_rgb[3 * p + 1] = h_vals[k].y; out_rgb[3 * p + 2] = h_vals[k].z; }
+        if (out_t) out_t[p] = h_vals[k].w;
+    }
+    if (tr)
+        std::fprintf(stderr, "[dropin] upload %.3f ms, render %.3f ms, readback %.3f ms, widen %.3f ms\n", t1 - t0,
+                     t2 - t1, t3 - t2, now_ms() - t3);
+    return PS_OK;
 }
 
 int ps_count_pairs(ps_ctx* c, const ps_scene* s, const ps_camera* cam, const ps_config* cfg,

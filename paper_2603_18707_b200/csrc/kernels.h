@@ -125,7 +125,9 @@ int launch_image_metrics(const void* rgb_a, const void* t_a, const void* rgb_b, 
                          int H, const double bg[3], void* scratch, ps_image_metrics* out, cudaStream_t st);
 
 // utils.cu
-void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st);
+// uploaded splat records (device; raw Splat3D or the drop-in's compact 280-B
+// record) -> upload staging (fp64 geometry planes + fp32 SH)
+void launch_split_records(const double* rec, int64_t n, bool raw, double* staging, float* sh, cudaStream_t st);
 // scene reordering along a 30-bit Morton curve of the means (upload time)
 void launch_morton_order(const double* means, int64_t n, unsigned long long* bb, uint32_t* keys, uint32_t* vals,
                          cudaStream_t st);

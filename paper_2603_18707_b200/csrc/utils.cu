@@ -1,5 +1,5 @@
-// utils.cu — small device helpers: on-device de-interleave of uploaded splat
-// arrays (so a host upload is a handful of large DMA copies), and the FP32
+// utils.cu — small device helpers: on-device split of uploaded Splat3D records
+// and the scene's Morton reordering (so a host upload is a handful of large DMA copies), and the FP32
 // issue-rate microbenchmark the bench uses as the blend roofline denominator.
 #include <algorithm>
 
@@ -9,16 +9,29 @@ namespace ps {
 
 namespace {
 
-// staging = [means n*3 | scales n*3 | rots n*4] (interleaved per splat)
-__global__ void k_deinterleave(const double* __restrict__ st, int64_t n, SceneDev s) {
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double* m = st + 3 * i;
-        const double* sc = st + 3 * n + 3 * i;
-        const double* r = st + 6 * n + 4 * i;
-        s.mean[0][i] = m[0]; s.mean[1][i] = m[1]; s.mean[2][i] = m[2];
-        s.scale[0][i] = sc[0]; s.scale[1][i] = sc[1]; s.scale[2][i] = sc[2];
-        s.rot[0][i] = r[0]; s.rot[1][i] = r[1]; s.rot[2][i] = r[2]; s.rot[3][i] = r[3];
+// Uploaded splat records -> the upload staging layout: geometry fp64
+// [means 3n | scales 3n | rots 4n | opacity n] and SH fp32 [n][48].
+//   RAW:  the reference's Splat3D (59 doubles: mean 3, scale 3, rotation 4,
+//         opacity, sh 48; projection.hpp:13-19), SH narrowed here;
+//   else: the drop-in's compact record (the same 11 doubles, then the 48 SH
+//         coefficients already rounded to fp32 on the host: 280 B).
+// Each thread moves one 8-byte word of the flat record array (coalesced reads).
+template <bool RAW>
+__global__ void k_split_records(const double* __restrict__ rec, int64_t n, double* __restrict__ st,
+                                float* __restrict__ sh) {
+    constexpr int W = RAW ? PS_SPLAT3D_DOUBLES : 11 + 24; // 8-byte words per record
+    const uint64_t total = static_cast<uint64_t>(n) * W;
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double v = rec[e];
+        const uint64_t i = e / W;
+        const int f = static_cast<int>(e - i * W);
+        if (f < 3) st[3 * i + f] = v;
+        else if (f < 6) st[3 * n + 3 * i + (f - 3)] = v;
+        else if (f < 10) st[6 * n + 4 * i + (f - 6)] = v;
+        else if (f == 10) st[10 * n + i] = v;
+        else if (RAW) sh[48 * i + (f - 11)] = __double2float_rn(v);
+        else reinterpret_cast<double*>(sh)[24 * i + (f - 11)] = v; // two fp32 coefficients
     }
 }
 
@@ -143,11 +156,13 @@ void launch_gather_scene(const double* staging, const double* opac, const float4
     k_gather_scene<<<blocks, 256, 0, st>>>(staging, opac, sh, perm, n, s);
 }
 
-void launch_deinterleave(const double* staging, int64_t n, const SceneDev& s, cudaStream_t st) {
+void launch_split_records(const double* rec, int64_t n, bool raw, double* staging, float* sh, cudaStream_t st) {
     if (n <= 0) return;
-    int blocks = static_cast<int>((n + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    k_deinterleave<<<blocks, 256, 0, st>>>(staging, n, s);
+    const int64_t total = n * (raw ? PS_SPLAT3D_DOUBLES : 35);
+    int blocks = static_cast<int>((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (raw) k_split_records<true><<<blocks, 256, 0, st>>>(rec, n, staging, sh);
+    else k_split_records<false><<<blocks, 256, 0, st>>>(rec, n, staging, sh);
 }
 
 // Returns achieved FP32 TFLOP/s (FFMA = 2 flops) over `reps` timed launches.

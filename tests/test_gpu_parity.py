@@ -149,3 +149,34 @@ def test_non_monotone_kernels(gpu, reference, sname, coeffs, kind):
     fb, ctr = gpu.render(splats, cam, cfg)
     assert ctr.as_dict() == ctr_r
     assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL
+
+
+def test_render_splat3d_dropin_sequence(gpu, reference):
+    """ps_render_splats reuses one device scene and the pinned upload ring across
+    calls: a sequence of different scenes (growing, shrinking, empty; chunk
+    boundaries of the 16 MB ring crossed by the 50k scene), counters on and off,
+    tile sizes 16 and 24, each against the reference's fp64 framebuffer."""
+    import ctypes as C
+    from paper_2603_18707_b200 import abi
+    from paper_2603_18707_b200._native import lib
+    seq = [("g", 1, 10000), ("g", 5, 50000), ("random", 2, 0), ("g", 7, 300), ("g", 1, 10000)]
+    for k, (kind, seed, n) in enumerate(seq):
+        splats, deg = scene(kind, seed, n)
+        if k == 3:
+            splats = splats[:0]
+        cam = camera(3, 200 + 8 * k, 150, k % 3)
+        cfg = config("poly1" if k % 2 == 0 else "exp",
+                     api.CullingMode.OpacityAware if k % 2 == 0 else api.CullingMode.StopThePop, deg,
+                     tile_size=16 if k != 2 else 24)
+        rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+        fb, ctr = gpu.render_splat3d(splats, cam, cfg)
+        assert ctr.as_dict() == ctr_r, k
+        assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL and max_abs(fb.transmittance, t_r) <= IMAGE_TOL, k
+        # counters NULL: the counter-free blend through the same drop-in call
+        a = np.ascontiguousarray(splats, dtype=np.float64)
+        rgb = np.zeros((cam.height, cam.width, 3))
+        tr = np.zeros((cam.height, cam.width))
+        c, g = cam.to_struct(), cfg.to_struct()
+        api._check(lib().ps_render_splats(gpu.handle, abi.dptr(a), len(a), C.byref(c), C.byref(g), abi.dptr(rgb),
+                                          abi.dptr(tr), None), gpu.handle)
+        assert max_abs(rgb, rgb_r) <= IMAGE_TOL and max_abs(tr, t_r) <= IMAGE_TOL, k
