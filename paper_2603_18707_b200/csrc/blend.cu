@@ -518,26 +518,28 @@ __device__ __forceinline__ void walk(Pair& p, uint32_t m, uint32_t rb, float yc,
     }
 }
 
-// alpha of (pixel (gx, gy), splat i) in the reference's exact fp64 arithmetic
-// (raster.cpp:262-271; see exact_alpha_ge_eps)
-__device__ __forceinline__ double exact_alpha(const BlendArgs& A, uint32_t i, double2 m, int gx, int gy) {
-    const double2 ab = A.conic_ab[i];
-    const double2 cq = A.conic_cq[i];
-    const double o = A.opacity_eff[i];
-    const double dx = dsub(dadd(static_cast<double>(gx), 0.5), m.x);
-    const double dy = dsub(dadd(static_cast<double>(gy), 0.5), m.y);
-    const double q = dadd(dadd(dmul(dmul(ab.x, dx), dx), dmul(dmul(dmul(2.0, ab.y), dx), dy)),
-                          dmul(dmul(cq.x, dy), dy));
-    const double v = dmul(o, eval_kernel_rn(A.P.cfg.kernel, q));
-    return (v < 0.999) ? v : 0.999;
-}
-
 // Exact replay of one flagged pixel by a whole warp (the reference's per-pixel
 // loop, raster.cpp:250-283, in fp64 with its operation order): alpha of 32 list
 // entries in parallel, then the transmittance chain serially over the accepted
 // ones. In quadric mode an entry with fp32 q > q_hi is certainly skipped by the
 // reference (the same certified test the fast path uses), so only candidates
-// reach the fp64 kernel evaluation.
+// reach the fp64 kernel evaluation. Each lane's records arrive in one memory
+// round trip, and the next 32 entries' are in flight during the chain.
+struct ReplayRec {
+    double2 m, ab, cq;
+    double o;
+    float4 b0, b1;
+    float2 b2;
+};
+
+__device__ __forceinline__ void replay_fetch(const BlendArgs& A, const uint32_t* list, int j, int L, ReplayRec& R) {
+    if (j < L) {
+        const uint32_t i = list[j];
+        R.m = A.mean2d[i]; R.ab = A.conic_ab[i]; R.cq = A.conic_cq[i]; R.o = A.opacity_eff[i];
+        R.b0 = A.bl0[i]; R.b1 = A.bl1[i]; R.b2 = A.bl2[i];
+    }
+}
+
 template <int MODE, bool COUNT>
 __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t* list, int L, int lxy, int px0,
                                           int py0, unsigned long long& ev, unsigned long long& bl) {
@@ -548,36 +550,35 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
     const double eps = A.P.cfg.epsilon, floor_t = A.P.cfg.transmittance_floor;
     double trans = 1.0, r = 0.0, g = 0.0, b = 0.0;
     unsigned long long evals = 0, blended = 0;
-    bool done = false;
-    for (int base = 0; base < L && !done; base += 32) {
+    ReplayRec R;
+    R.b0 = make_float4(0.f, 0.f, 0.f, -1.f);
+    replay_fetch(A, list, lane, L, R);
+    for (int base = 0; base < L; base += 32) {
         const int j = base + lane;
         double alpha = 0.0;
-        float cr = 0.f, cg = 0.f, cb = 0.f;
         bool acc = false;
         if (j < L) {
-            const uint32_t i = list[j];
-            const double2 m = A.mean2d[i];
             bool cand = true;
             if (MODE == kQuadricThreshold) {
-                const float4 b0 = A.bl0[i];
-                const float mx = static_cast<float>(m.x - px0), my = static_cast<float>(m.y - py0);
+                const float mx = static_cast<float>(R.m.x - px0), my = static_cast<float>(R.m.y - py0);
                 const float dy = yc - my;
-                const float u = xc - fmaf(-b0.y, dy, mx);
-                const float q = fmaf(b0.x * u, u, b0.z * dy * dy);
-                cand = q <= b0.w;
+                const float u = xc - fmaf(-R.b0.y, dy, mx);
+                const float q = fmaf(R.b0.x * u, u, R.b0.z * dy * dy);
+                cand = q <= R.b0.w;
             }
             if (cand) {
-                alpha = exact_alpha(A, i, m, gx, gy);
+                const double dx = dsub(dadd(static_cast<double>(gx), 0.5), R.m.x);
+                const double dy = dsub(dadd(static_cast<double>(gy), 0.5), R.m.y);
+                const double q = dadd(dadd(dmul(dmul(R.ab.x, dx), dx), dmul(dmul(dmul(2.0, R.ab.y), dx), dy)),
+                                      dmul(dmul(R.cq.x, dy), dy));
+                const double v = dmul(R.o, eval_kernel_rn(A.P.cfg.kernel, q));
+                alpha = (v < 0.999) ? v : 0.999;
                 acc = !(alpha < eps);
-                if (acc) {
-                    const float4 b1 = A.bl1[i];
-                    const float2 b2 = A.bl2[i];
-                    cr = b1.w; cg = b2.x; cb = b2.y;
-                }
             }
         }
+        const float cr = R.b1.w, cg = R.b2.x, cb = R.b2.y;
+        replay_fetch(A, list, base + 32 + lane, L, R); // next 32 entries, in flight during the chain
         uint32_t mask = __ballot_sync(0xffffffffu, acc);
-        const int nvalid = min(32, L - base);
         int stop = -1;
         while (mask) {
             const int src = __ffs(mask) - 1;
@@ -594,10 +595,9 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
         }
         if (stop >= 0) {
             evals += static_cast<unsigned long long>(stop) + 1;
-            done = true;
-        } else {
-            evals += static_cast<unsigned long long>(nvalid);
+            break;
         }
+        evals += static_cast<unsigned long long>(min(32, L - base));
     }
     if (lane == 0) {
         const size_t pix = static_cast<size_t>(gy) * A.P.cam.width + gx;

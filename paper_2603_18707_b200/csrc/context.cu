@@ -508,7 +508,9 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
         return run_frame(c, s, cam, cfg_in, sized, res);
     }
     frame_stats(c, res);
-    c->clean_tiles = res.published; // the blend zeroed the counters and tile counts
+    // K7's last CTA zeroed the counters, the blend's CTAs the frame's tile counts
+    const int64_t ts = cfg_in.tile_size;
+    c->clean_tiles = res.published ? ((cam.width + ts - 1) / ts) * ((cam.height + ts - 1) / ts) : 0;
     return PS_OK;
 }
 
