@@ -258,7 +258,7 @@ constexpr int kB16 = 128;
 constexpr float kNaNf = __builtin_nanf("");
 // byte offsets of the record planes a, b, c, d in the staging area
 constexpr int kRecs = kB16;
-constexpr uint32_t kOffB = kRecs * 16, kOffC = 2 * kRecs * 16, kOffD = 3 * kRecs * 16;
+constexpr uint32_t kOffB = kRecs * 16, kOffC = 2 * kRecs * 16, kOffD = 3 * kRecs * 16, kOffE = 4 * kRecs * 16;
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
     float4 v;
@@ -330,9 +330,20 @@ __device__ __forceinline__ uint32_t row_pairs(int row, float mx, float my, float
     return (0xFFu << lo) & (0xFFu >> (7 - hi));
 }
 
-// Shared-memory record of one staged splat (tile-local, fp32):
-//   a = {mx, my, A, beta}  b = {gamma, q_hi, q_lo, g'}  c = {-K0, -r, -g, -b}
-//   d = {-K1, -K2, -K3, -}
+// Record-local split of a tile-local coordinate v (see the record layout below).
+__device__ __forceinline__ void split_local(double v, float& o, float& r) {
+    o = rintf(static_cast<float>(v));
+    r = static_cast<float>(v - static_cast<double>(o));
+}
+
+// Shared-memory record of one staged splat (fp32):
+//   a = {mx', my', A, beta}  b = {gamma, q_hi, q_lo, g'}  c = {-K0, -r, -g, -b}
+//   d = {ox, oy, -K1, -K2}   e = {-K3, -, -, -}
+// Record-local coordinates: the tile-local mean is (ox + mx', oy + my') with
+// (ox, oy) = rint of it (exact small integers) and |mx'|, |my'| <= 1/2, so a
+// pixel's offset x - ox is exact and no rounding error scales with the
+// position inside the tile (exact_kernels.cu blend_record bounds q's error
+// for exactly this arithmetic: split_local / record_q).
 // K_j = o c_j folds the opacity into the polynomial (c.x = log2 o for exp; -o
 // in alpha-threshold mode). The walk carries NEGATED alphas (-alpha = Horner
 // over the negated coefficients, exactly), so that T' = fma(-alpha, T, T) is
@@ -376,10 +387,13 @@ __device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const Fr
     const float4 a = lds128(rec);
     const float4 b = lds128(rec + kOffB);
     const float4 c = lds128(rec + kOffC);
-    const float dy = yc - a.y;
-    const float mr = fmaf(-a.w, dy, a.x);
+    const float4 d = lds128(rec + kOffD);
+    // q = A u^2 + gamma dy^2 in record-local coordinates: dy = (yc - oy) - my',
+    // u = (x - ox) + (beta dy - mx') (yc - oy and x - ox are exact)
+    const float dy = (yc - d.y) - a.y;
+    const float tt = fmaf(a.w, dy, -a.x);
     const float cr = b.x * dy * dy;
-    const F2 u = f2sub(x, f2b(mr));
+    const F2 u = f2add(f2sub(x, f2b(d.x)), f2b(tt));
     const F2 q = f2fma(f2mul(u, f2b(a.z)), u, f2b(cr));
     const float q0 = f2lo(q), q1 = f2hi(q);
     Frag f;
@@ -398,12 +412,11 @@ __device__ __forceinline__ Frag pair_frag(F2 x, uint32_t rec, float yc, const Fr
             const F2 ar = f2fma(q, f2b(-0.72134752044448170f), f2b(c.x));
             na = f2(-ex2_approx(f2lo(ar)), -ex2_approx(f2hi(ar)));
         } else if (ORDER == 1) {
-            na = f2fma(q, f2b(lds32(rec + kOffD)), f2b(c.x));
+            na = f2fma(q, f2b(d.z), f2b(c.x));
         } else {
-            const float4 d = lds128(rec + kOffD);
-            F2 pq = f2b(ORDER == 2 ? d.y : d.z);
-            if (ORDER >= 3) pq = f2fma(pq, q, f2b(d.y));
-            pq = f2fma(pq, q, f2b(d.x));
+            F2 pq = f2b(ORDER == 2 ? d.w : lds32(rec + kOffE));
+            if (ORDER >= 3) pq = f2fma(pq, q, f2b(d.w));
+            pq = f2fma(pq, q, f2b(d.z));
             na = f2fma(pq, q, f2b(c.x));
         }
         f.n0 = CLAMP ? fmaxf(-0.999f, f2lo(na)) : f2lo(na);
@@ -560,9 +573,13 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
         if (j < L) {
             bool cand = true;
             if (MODE == kQuadricThreshold) {
-                const float mx = static_cast<float>(R.m.x - px0), my = static_cast<float>(R.m.y - py0);
-                const float dy = yc - my;
-                const float u = xc - fmaf(-R.b0.y, dy, mx);
+                // the walk's arithmetic (pair_frag), so the same certified bound applies
+                float ox, oy, mxr, myr;
+                split_local(R.m.x - px0, ox, mxr);
+                split_local(R.m.y - py0, oy, myr);
+                const float dy = (yc - oy) - myr;
+                const float tt = fmaf(R.b0.y, dy, -mxr);
+                const float u = (xc - ox) + tt;
                 const float q = fmaf(R.b0.x * u, u, R.b0.z * dy * dy);
                 cand = q <= R.b0.w;
             }
@@ -647,12 +664,13 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     __shared__ __align__(16) uint32_t S[SortSm::WORDS];
     __shared__ uint32_t s_nflag;
     __shared__ uint16_t s_flag[256];
-    static_assert(4 * kRecs * 16 + 4 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
+    static_assert(5 * kRecs * 16 + 4 * kB16 * 4 <= SortSm::LIST * 4, "staging overlaps the sorted list");
     float4* sA = reinterpret_cast<float4*>(S);
     float4* sB = sA + kRecs;
     float4* sC = sA + 2 * kRecs;
     float4* sD = sA + 3 * kRecs;
-    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 4 * kRecs); // [warp][record]
+    float4* sE = sA + 4 * kRecs;
+    uint32_t (*cover)[kB16] = reinterpret_cast<uint32_t (*)[kB16]>(sA + 5 * kRecs); // [warp][record]
     const uint32_t s_rec = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
 
     if (A.zero_counts && threadIdx.x == 0) A.zero_counts[blockIdx.x] = 0u; // K3's cursors are dead
@@ -706,7 +724,11 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
         if (__syncthreads_count(live) == 0) break;
         bool needs_clamp;
         {   // stage the record prefetched for this batch
-            const float mx = static_cast<float>(pm.x - px0), my = static_cast<float>(pm.y - py0);
+            const double lxd = pm.x - px0, lyd = pm.y - py0;
+            const float mx = static_cast<float>(lxd), my = static_cast<float>(lyd); // coverage only
+            float ox, oy, mxr, myr;
+            split_local(lxd, ox, mxr);
+            split_local(lyd, oy, myr);
             const float Aq = pb0.x, beta = pb0.y, gamma = pb0.z, qhi = pb0.w;
             const float o = pb1.y, ga = pb1.z;
             float K0 = o, K1 = 0.f, K2 = 0.f, K3 = 0.f;
@@ -718,10 +740,11 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
             // kernel is non-increasing in q >= 0, so alpha <= alpha(0) = K0, resp.
             // 2^K0 = o for exp; the margin covers fp32 Horner rounding)
             needs_clamp = t < L - base && (MODE != kQuadricThreshold || (KIND == 0 ? pb1.y >= -1.6e-3f : K0 >= 0.9989f));
-            sA[t] = make_float4(mx, my, Aq, beta);
+            sA[t] = make_float4(mxr, myr, Aq, beta);
             sB[t] = make_float4(gamma, qhi, pb1.x, gp);
             sC[t] = make_float4(KIND == 0 ? pb1.y : -K0, -pb1.w, -pb2.x, -pb2.y);
-            sD[t] = make_float4(-K1, -K2, -K3, 0.f);
+            sD[t] = make_float4(ox, oy, -K1, -K2);
+            if (ORDER >= 3) sE[t].x = -K3;
             // coverage of {q <= q_hi}: word w = 8 rows x 4 pairs of warp w's block
             uint32_t cw[4] = {0u, 0u, 0u, 0u};
             const bool full = MODE != kQuadricThreshold || !(qhi < 3.0e38f) || !(Aq > 0.0f) ||

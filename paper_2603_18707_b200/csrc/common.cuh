@@ -132,6 +132,8 @@ struct FrameParams {
     int bound_class;        // K1a specialisation (culling mode x bound kernel)
     int blend_class;        // K1b specialisation (blend kernel)
     double campos[3];       // Camera::position() (projection.hpp:29), computed on the host
+    double root_slack;      // polynomial blend kernels: the reference's alpha64 rounding near eps in
+                            // q units (host_root_slack); 0 for exp
 };
 
 #define PS_CUDA_TRY(expr)                                                  \

@@ -39,6 +39,7 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 int host_validate_config(const ps_config& c);
 int host_validate_camera(const ps_camera& c);
 int host_kernel_threshold_mode(const ps_kernel& k);
+double host_root_slack(const ps_kernel& k);
 int host_effective_terms(const ps_kernel& k);
 void host_camera_position(const ps_camera& cam, double out[3]);
 
@@ -422,6 +423,7 @@ int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode m
     const int sh_floats = 3 * (sh_deg + 1) * (sh_deg + 1);
     P.sh_floats4 = (sh_floats + 3) / 4;
     P.threshold_mode = host_kernel_threshold_mode(cfg.kernel);
+    P.root_slack = host_root_slack(cfg.kernel);
     P.kf.kind = cfg.kernel.kind;
     P.kf.order = cfg.kernel.order;
     for (int j = 0; j < 4; ++j) P.kf.c[j] = static_cast<float>(cfg.kernel.coeffs[j]);

@@ -135,23 +135,53 @@ __device__ void blend_record(double a, double b, double c, double o, const Frame
         // blends it is replayed exactly
         qhi = INFINITY; qlo = -INFINITY; eT = INFINITY;
     } else {
-        double qb = (th == 1 ? 1.25 * qs : 25.0) + 1.0;
-        double U = sqrt(qb / a), D = sqrt(qb / gamma);
-        double ab_ = fabs(beta);
-        double X = U + ab_ * D;
-        double dmx = e32 * (X + ts), dmy = e32 * (D + ts);
-        double ddx = dmx + e32 * X, ddy = dmy + e32 * D;
-        double gam_rel = e32 + 4.0 * e64 * (c + b * b / a) / gamma;
-        // u is formed either as (dx + beta dy) or as x - (mx - beta dy); bound both
-        double du = 2.0 * dmx + ddx + ab_ * ddy + 2.0 * e32 * ab_ * D + e32 * (U + X);
-        double dr = qb * (2.0 * e32 + gam_rel) + 2.0 * gamma * D * ddy;
-        double dau = qb * 3.0 * e32 + 2.0 * a * U * du;
-        double dq = e32 * qb + dau + dr;
-        double ref = 8.0 * e64 * (a * X * X + 2.0 * fabs(b) * X * D + c * D * D) +
-                     4.0 * e64 * (a * X + fabs(b) * D) * (X + D);
-        // each term above is a first-order upper bound; 1.25 covers the
-        // second-order products, 1e-7 qb the root-finding / alpha64 rounding
-        double Gq = 1.25 * (dq + ref) + 1e-7 * qb + 1e-12;
+        // Gq(qb): bound on |q_fp32 - q_ref| over the region q <= qb
+        auto gq_for = [&](double qb) -> double {
+            double U = sqrt(qb / a), D = sqrt(qb / gamma);
+            double ab_ = fabs(beta);
+            double X = U + ab_ * D;
+            double gam_rel = e32 + 4.0 * e64 * (c + b * b / a) / gamma;
+            double du, ddy;
+            if (P.cfg.tile_size == 16) {
+                // k_blend16 (blend.cu pair_frag) works in record-local coordinates:
+                // the tile-local mean m = o + m' with o = rint(m) (integer, exact)
+                // and |m'| <= M = 0.5 + e32 (X + ts) held in fp32 (error e32 M);
+                // dy = (yc - oy) - my' (yc - oy exact), t = fma(beta, dy, -mx'),
+                // u = (x - ox) + t (x - ox exact), so no term scales with the tile
+                const double Mx = 0.5 + e32 * (X + ts), My = 0.5 + e32 * (D + ts);
+                const double dmx = e32 * Mx, dmy = e32 * My;
+                ddy = dmy + e32 * D;
+                du = ab_ * ddy + e32 * ab_ * D + dmx + e32 * (ab_ * D + Mx) + e32 * U;
+            } else {
+                // k_blend: tile-local fp32 mean (error e32 (X + ts))
+                const double dmx = e32 * (X + ts), dmy = e32 * (D + ts);
+                const double ddx = dmx + e32 * X;
+                ddy = dmy + e32 * D;
+                // u is formed either as (dx + beta dy) or as x - (mx - beta dy); bound both
+                du = 2.0 * dmx + ddx + ab_ * ddy + 2.0 * e32 * ab_ * D + e32 * (U + X);
+            }
+            double dr = qb * (2.0 * e32 + gam_rel) + 2.0 * gamma * D * ddy;
+            double dau = qb * 3.0 * e32 + 2.0 * a * U * du;
+            double dq = e32 * qb + dau + dr;
+            double ref = 8.0 * e64 * (a * X * X + 2.0 * fabs(b) * X * D + c * D * D) +
+                         4.0 * e64 * (a * X + fabs(b) * D) * (X + D);
+            // each term above is a first-order upper bound; 1.25 covers the
+            // second-order products. The threshold q*: a polished fp64 root
+            // (~1e-15 relative; 1e-9 qb) and, for polynomials, the reference's
+            // fp64 rounding of o p(q) near eps in q units (P.root_slack)
+            const double droot = 1e-9 * qb + (th == 1 ? P.root_slack : 0.0);
+            return 1.25 * (dq + ref) + droot + 1e-12;
+        };
+        // quadric mode: a candidate has fp32 q <= q_hi = fl_up(q* + Gq), so its
+        // true q is below q* + 2 Gq (+ one fp32 ulp) and a region just above q*
+        // suffices; otherwise (or if that region turns out too tight) q <= 1.25 q* + 1
+        const bool tight = th == 1 && P.threshold_mode == kQuadricThreshold;
+        double qb = tight ? 1.01 * qs + 0.01 : (th == 1 ? 1.25 * qs : 25.0) + 1.0;
+        double Gq = gq_for(qb);
+        if (tight && !((qs + Gq) * (1.0 + 2.5e-7) + Gq <= qb)) {
+            qb = 1.25 * qs + 1.0;
+            Gq = gq_for(qb);
+        }
         // |alpha_fp32 - alpha_ref| for accepted fragments (q <= qb):
         //   o max|k'| Gq  +  evaluation rounding  (+ ex2.approx error for exp)
         double kp = 0.5, kmag = 1.0, extra = 0.0;

@@ -75,6 +75,38 @@ int host_kernel_threshold_mode(const ps_kernel& k) {
     return 0;
 }
 
+// Quadric-threshold mode, polynomial kernel: the reference decides alpha >= eps
+// from o p(q) evaluated in fp64 (Horner, order + 1 roundings, plus the eps / o
+// division of the shifted root problem), so near the threshold its decision
+// can differ from q <= q* by at most 8 u64 (sum |c_j| q^j + 1) / |p'(q)| in q.
+// Over q in [0, R] (R: first root of p; q* < R) that is bounded by this
+// constant (infinite when p' vanishes on [0, R]).
+double host_root_slack(const ps_kernel& k) {
+    if (k.kind == PS_KERNEL_EXPONENTIAL) return 0.0;
+    const double R = k.first_root;
+    if (!(R > 0.0) || !std::isfinite(R)) return INFINITY;
+    const double d0 = k.order >= 1 ? k.coeffs[1] : 0.0;
+    const double d1 = k.order >= 2 ? 2.0 * k.coeffs[2] : 0.0;
+    const double d2 = k.order >= 3 ? 3.0 * k.coeffs[3] : 0.0;
+    auto dval = [&](double q) { return d0 + d1 * q + d2 * q * q; };
+    double lo = std::fmin(std::fabs(dval(0.0)), std::fabs(dval(R)));
+    if (dval(0.0) * dval(R) <= 0.0) lo = 0.0;
+    if (d2 != 0.0) {
+        const double qv = -d1 / (2.0 * d2);
+        if (qv > 0.0 && qv < R) {
+            if (dval(qv) * dval(0.0) <= 0.0) lo = 0.0;
+            lo = std::fmin(lo, std::fabs(dval(qv)));
+        }
+    }
+    if (!(lo > 0.0)) return INFINITY;
+    double mag = 0.0, qp = 1.0;
+    for (int j = 0; j <= k.order; ++j) {
+        mag += std::fabs(k.coeffs[j]) * qp;
+        qp *= R;
+    }
+    return 1.1 * 8.0 * 1.1102230246251565e-16 * (mag + 1.0) / lo;
+}
+
 } // namespace ps
 
 using namespace ps;

@@ -30,6 +30,8 @@ ap.add_argument("--mode", default="OpacityAware")
 ap.add_argument("--tiles", type=int, default=1, help="model every k-th tile")
 ap.add_argument("--scale-gq", type=float, default=1.0)
 ap.add_argument("--scale-ga", type=float, default=1.0)
+ap.add_argument("--old", action="store_true", help="round-1 bound (tile-local coordinates, 1e-7 qb)")
+ap.add_argument("--centre", action="store_true", help="tile-local arithmetic with the origin at the tile centre")
 ap.add_argument("--slack", type=float, default=3.2, help="g' = 1.001 (g + slack u) + 4 u64")
 a = ap.parse_args()
 
@@ -64,21 +66,34 @@ else:
         rts = np.roots(c[::-1])
         rts = rts[(np.abs(rts.imag) < 1e-12) & (rts.real > 0)].real
         qs[i] = rts.min() if len(rts) else 25.0
-qb = 1.25 * qs + 1.0
+qb = 1.25 * qs + 1.0 if a.old else 1.01 * qs + 0.01
 U, D = np.sqrt(qb / ca), np.sqrt(qb / gamma)
 ab_ = np.abs(beta)
 X = U + ab_ * D
 ts = 16.0
-dmx, dmy = e32 * (X + ts), e32 * (D + ts)
-ddx, ddy = dmx + e32 * X, dmy + e32 * D
 gam_rel = e32 + 4.0 * e64 * (cc + cb * cb / ca) / gamma
-du = 2.0 * dmx + ddx + ab_ * ddy + 2.0 * e32 * ab_ * D + e32 * (U + X)
+if a.old or a.centre:
+    tsx = ts / 2 if a.centre else ts
+    dmx, dmy = e32 * (X + tsx), e32 * (D + tsx)
+    ddx, ddy = dmx + e32 * X, dmy + e32 * D
+    du = 2.0 * dmx + ddx + ab_ * ddy + 2.0 * e32 * ab_ * D + e32 * (U + X)
+else:
+    Mx, My = 0.5 + e32 * (X + ts), 0.5 + e32 * (D + ts)
+    dmx, dmy = e32 * Mx, e32 * My
+    ddy = dmy + e32 * D
+    du = ab_ * ddy + e32 * ab_ * D + dmx + e32 * (ab_ * D + Mx) + e32 * U
 dr = qb * (2.0 * e32 + gam_rel) + 2.0 * gamma * D * ddy
 dau = qb * 3.0 * e32 + 2.0 * ca * U * du
 dq = e32 * qb + dau + dr
 refe = 8.0 * e64 * (ca * X * X + 2.0 * np.abs(cb) * X * D + cc * D * D) + 4.0 * e64 * (ca * X + np.abs(cb) * D) * (X + D)
-Gq_terms = {"dau(u)": 1.25 * dau, "dr(row)": 1.25 * dr, "e32 qb": 1.25 * e32 * qb, "1e-7 qb": 1e-7 * qb, "ref": 1.25 * refe}
-Gq = (1.25 * (dq + refe) + 1e-7 * qb + 1e-12) * a.scale_gq
+if a.old or expk:
+    droot = (1e-7 if a.old else 1e-9) * qb
+else:
+    pd = sum((j + 1) * coef[j + 1] * qs ** j for j in range(k.order))
+    mag = sum(np.abs(coef[j]) * qs ** j for j in range(k.order + 1))
+    droot = 1e-9 * qb + 8.0 * e64 * (mag + eps / o) / np.maximum(np.abs(pd), 1e-300)
+Gq = (1.25 * (dq + refe) + droot + 1e-12) * a.scale_gq
+Gq_terms = {"dau(u)": 1.25 * dau, "dr(row)": 1.25 * dr, "e32 qb": 1.25 * e32 * qb, "droot": droot, "ref": 1.25 * refe}
 amax = np.minimum(o if expk else o * coef[0], 0.999)
 if expk:
     kp, kmag = 0.5, 0.0

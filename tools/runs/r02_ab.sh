@@ -1,0 +1,2 @@
+# A/B of the _ab/*.so variants at C2 (poly1 / exp), stage medians
+tools/ab_quick.sh 2>&1 | grep -v "^{"; tools/ab_quick.sh --kernel exp --mode StopThePop 2>&1 | grep -v "^{"
