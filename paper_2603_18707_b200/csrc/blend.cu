@@ -639,13 +639,17 @@ __device__ __forceinline__ void replay_pixel(const BlendArgs& A, const uint32_t*
 // memory) and zeroes them for the next frame (which then needs no memset):
 // every CTA's counter atomics are fenced before it counts itself done.
 __device__ __forceinline__ void publish_counters(const BlendArgs& A) {
+    static_assert(sizeof(DevCounters) % 4 == 0 && sizeof(DevCounters) / 4 <= 32, "one word per lane of warp 0");
     if (!A.publish) return;
-    __threadfence();
-    __syncthreads();
-    __shared__ bool s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&A.ctr->done_ctas, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (s_last && threadIdx.x < sizeof(DevCounters) / 4) {
+    __syncthreads(); // the CTA's counter atomics precede thread 0's release below (barrier + fence cumulativity)
+    if (threadIdx.x >= 32) return;
+    bool last = false;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&A.ctr->done_ctas, 1u) == gridDim.x - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && threadIdx.x < sizeof(DevCounters) / 4) {
         __threadfence();
         volatile uint32_t* src = reinterpret_cast<volatile uint32_t*>(A.ctr);
         reinterpret_cast<volatile uint32_t*>(A.publish)[threadIdx.x] = src[threadIdx.x];
@@ -907,7 +911,6 @@ int launch_blend(const FrameDev& f, const FrameParams& P, const uint32_t* pair_v
     if (n_tiles == 0) return 0;
     if (ts == 16) {
         if (publish && published) {
-            static_assert(sizeof(DevCounters) % 4 == 0 && sizeof(DevCounters) / 4 <= 128, "one word per thread");
             a.publish = publish;
             a.zero_counts = f.tile_count;
             *published = static_cast<uint32_t>(n_tiles);

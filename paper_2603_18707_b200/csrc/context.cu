@@ -607,8 +607,14 @@ int run_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_confi
         BlendOut out{req.d_rgb, req.d_t};
         bool replay_fused = false;
         c->h_ctr->done_ctas = 0xffffffffu; // poisoned until the blend's last CTA publishes
+#ifdef PS_AB_PRESORT
+        launch_tile_sort(f, s->dev.orig, n_tiles, cap, c->d_ctr, strm, &launches);
+        launches += launch_blend(f, P, f.pval, nullptr, cap, s->dev.orig, c->d_ctr, out, req.count_work, strm,
+                                 &replay_fused, c->h_ctr, &res.published);
+#else
         launches += launch_blend(f, P, f.pval, f.pval, cap, s->dev.orig, c->d_ctr, out, req.count_work, strm,
                                  &replay_fused, c->h_ctr, &res.published);
+#endif
         record(c, 6);
         record(c, 7);
         if (!res.published)

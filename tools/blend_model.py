@@ -45,6 +45,8 @@ tx_n = (a.w + ts - 1) // ts
 ty_n = (a.h + ts - 1) // ts
 ly, lx = np.mgrid[0:16, 0:16]
 stats = []
+group_stats = []
+quad_stats = []
 step = a.tiles if a.tiles > 0 else 1
 for t in range(0, tx_n * ty_n, step):
     lst = idx[off[t]:off[t + 1]]
@@ -80,8 +82,25 @@ for t in range(0, tx_n * ty_n, step):
     # pixel pairs (2k, 2k+1) of each row: the walk's step set is the union
     c2 = cand.reshape(L, 16, 8, 2)
     pair_steps = (c2[..., 0] | c2[..., 1]).sum(axis=0)  # [16 rows, 8 pairs]
+    c4 = cand.reshape(L, 16, 4, 4).any(axis=3)           # 1x4 quads: [L, 16 rows, 4 quads]
+    q14 = c4.sum(axis=0)
+    c22 = cand.reshape(L, 8, 2, 8, 2).any(axis=(2, 4))   # 2x2 quads: [L, 8, 8]
+    q22 = c22.sum(axis=0)
+    # 1x4: warp = 8 rows x 4 quads (half tile); SIMT max per warp
+    w14 = [int(q14[h * 8:(h + 1) * 8].max()) for h in range(2)]
+    w22 = [int(q22[(h >> 1) * 4:(h >> 1) * 4 + 4, (h & 1) * 4:(h & 1) * 4 + 4].max()) for h in range(4)]
+    quad_stats.append((int(q14.sum()), sum(w14), int(q22.sum()), sum(w22)))
     # warp blocks: rows (w>>1)*8.., pairs (w&1)*4..
     ws = [pair_steps[(w >> 1) * 8:(w >> 1) * 8 + 8, (w & 1) * 4:(w & 1) * 4 + 4] for w in range(4)]
+    # per group of 32 records: the warp's step count is the max over its lanes
+    pc = (c2[..., 0] | c2[..., 1])                       # [L, 16, 8] pair candidates
+    ng = (L + 31) // 32
+    pcg = np.zeros((ng * 32, 16, 8), bool)
+    pcg[:L] = pc
+    per_g = pcg.reshape(ng, 32, 16, 8).sum(axis=1)       # [ng, 16, 8]
+    gmax = sum(int(per_g[:, (w >> 1) * 8:(w >> 1) * 8 + 8, (w & 1) * 4:(w & 1) * 4 + 4].reshape(ng, -1).max(axis=1).sum())
+               for w in range(4))
+    group_stats.append(gmax)
     evals = np.where(inside, np.minimum(term + 1, L), 0).sum()
     blended = (acc & live & inside[None, :]).sum()
     last = int(np.where(inside, np.minimum(term + 1, L), 0).max())   # entries the tile needs
@@ -115,6 +134,13 @@ print(f"warp walk steps (max over lanes) {wmax.sum()}  lane-steps {wsum.sum()}  
       f"SIMT efficiency {wsum.sum() / (32 * wmax.sum()):.3f}")
 print(f"per tile: L mean {L.mean():.0f} p50 {np.median(L):.0f} p99 {np.percentile(L, 99):.0f} max {L.max()}; "
       f"warp max steps per tile (max over warps): p50 {np.median(wmax.max(1)):.0f} max {wmax.max()}")
+gm = np.array(group_stats)
+print(f"warp walk steps with the SIMT max taken per 32-record group: {gm.sum()} (SIMT {wsum.sum() / (32 * gm.sum()):.3f})")
+qs_ = np.array(quad_stats)
+print(f"1x4 quad steps {qs_[:, 0].sum()} (x{qs_[:, 0].sum() * 4 / cand.sum():.3f} slots/cand), warp max-steps {qs_[:, 1].sum()} "
+      f"(2 warps/tile, SIMT {qs_[:, 0].sum() / (32 * qs_[:, 1].sum()):.3f})")
+print(f"2x2 quad steps {qs_[:, 2].sum()} (x{qs_[:, 2].sum() * 4 / cand.sum():.3f} slots/cand), warp max-steps {qs_[:, 3].sum()} "
+      f"(4 warps x 16 quads: SIMT {qs_[:, 2].sum() / (16 * qs_[:, 3].sum()):.3f})")
 np.savez_compressed(os.path.join(ROOT, "gpurun_out", f"blend_model_{a.kernel}_{a.mode}.npz"), L=L, last=last,
                     cand=cand, psteps=psteps, wmax=wmax, wsum=wsum, ev=ev, bl=bl,
                     tile=np.array([s[0] for s in stats]))

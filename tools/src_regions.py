@@ -17,12 +17,16 @@ def find(pat, start=0):
 
 k = find(r"__global__ void __launch_bounds__\(128, .*\) k_blend16")
 ranges = {
-    "walk": (find(r"^struct Frag \{"), find(r"^// alpha of \(pixel")),
-    "stage+cover": (find(r"stage the record prefetched", k), find(r"prefetch the next batch", k)),
-    "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Shared-memory record")),
+    "walk": (find(r"^struct Frag \{"), find(r"^// Exact replay of one flagged pixel")),
+    "replay": (find(r"^// Exact replay of one flagged pixel"), find(r"^// CAPR: rounds")),
+    "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Record-local split")),
     "transpose": (find(r"warp_transpose32\(uint32_t x"), find(r"^// ---- packed fp32 pairs")),
-    "group loop": (find(r"for \(int g = 0; g < kB16 / 32", k), find(r"unsigned long long ev = 0, bl = 0;", k)),
-    "replay": (find(r"^// alpha of \(pixel"), find(r"^template <int KIND, int ORDER, int MODE, bool COUNT", k - 6)),
+    "blend16 prologue": (k, find(r"for \(int base = 0; base < L; base \+= kB16\)", k)),
+    "batch barrier+stage": (find(r"for \(int base = 0; base < L; base \+= kB16\)", k), find(r"coverage of \{q <= q_hi\}", k)),
+    "stage cover loop": (find(r"coverage of \{q <= q_hi\}", k), find(r"__syncthreads_or\(needs_clamp\)", k)),
+    "barrier+prefetch": (find(r"__syncthreads_or\(needs_clamp\)", k), find(r"const int cnt = min\(kB16", k)),
+    "group loop": (find(r"const int cnt = min\(kB16", k), find(r"unsigned long long ev = 0, bl = 0;", k)),
+    "epilogue": (find(r"unsigned long long ev = 0, bl = 0;", k), find(r"^template <int KIND, int ORDER, int MODE>", k)),
 }
 hdr = next(r for r in rows if r and r[0] == "Line No")
 si, ii = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
