@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(1024) k_blend(const BlendArgs A) {
 // decisions the fp32 error bounds cannot certify are replayed at the end of the
 // CTA in exact fp64 from the tile's sorted list.
 constexpr int kB16 = 128;
+
 constexpr float kNaNf = __builtin_nanf("");
 // byte offsets of the record planes a, b, c, d in the staging area
 constexpr int kRecs = kB16;
@@ -707,25 +708,42 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     const int L = static_cast<int>(range.y - range.x);
     // the tile's list in (depth, index) order: sorted here for buckets that fit
     // one CTA, presorted in global memory otherwise
+    // (only its first P.sort_prefix positions, exactly: tiles terminate after
+    // ~200 entries at C2; the rest is sorted when a batch or the replay needs it)
     const uint32_t* list = A.pval + range.x;
-    if (A.pval_w && L > 1 && L <= SortSm::CAP) {
-        list = sort_one_tile<128, CAPR, false>(range, A.pval_w, A.pkey, A.key, A.orig, S,
-                                                              &A.ctr->unsorted);
+    int ranked = L;
+    const bool sort_here = A.pval_w && L > 1 && L <= SortSm::CAP;
+    if (sort_here) {
+        list = sort_one_tile<128, CAPR, false>(range, A.pval_w, A.pkey, A.key, A.orig, S, &A.ctr->unsorted,
+                                               max(P.sort_prefix, kB16), &ranked);
         __syncthreads();
     }
+    auto sort_all = [&]() { // the whole bucket (the staging area is dead when this runs)
+        list = sort_one_tile<128, CAPR, false>(range, A.pval_w, A.pkey, A.key, A.orig, S, &A.ctr->unsorted);
+        ranked = L;
+        __syncthreads();
+    };
     double2 pm = make_double2(0.0, 0.0);
     float4 pb0 = make_float4(0.f, 0.f, 0.f, -1.f), pb1 = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 pb2 = make_float2(0.f, 0.f);
-    if (t < L) {
-        const uint32_t pi = list[t];
-        pm = A.mean2d[pi];
-        pb0 = A.bl0[pi];
-        pb1 = A.bl1[pi];
-        pb2 = A.bl2[pi];
-    }
+    auto fetch = [&](int j) {
+        if (j < L) {
+            const uint32_t pi = list[j];
+            pm = A.mean2d[pi];
+            pb0 = A.bl0[pi];
+            pb1 = A.bl1[pi];
+            pb2 = A.bl2[pi];
+        }
+    };
+    fetch(t); // the ranked prefix holds at least the first batch
+    bool fetched = true;
     for (int base = 0; base < L; base += kB16) {
         const bool live = (f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x));
         if (__syncthreads_count(live) == 0) break;
+        if (!fetched) { // this batch lies beyond the sorted prefix (rare)
+            sort_all();
+            fetch(base + t);
+        }
         bool needs_clamp;
         {   // stage the record prefetched for this batch
             const double lxd = pm.x - px0, lyd = pm.y - py0;
@@ -774,13 +792,8 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
         }
         const bool clamp = __syncthreads_or(needs_clamp) != 0;
         const int nb = base + kB16;
-        if (nb + t < L) { // prefetch the next batch while this one is blended
-            const uint32_t pi = list[nb + t];
-            pm = A.mean2d[pi];
-            pb0 = A.bl0[pi];
-            pb1 = A.bl1[pi];
-            pb2 = A.bl2[pi];
-        }
+        fetched = nb + kB16 <= ranked || ranked == L;
+        if (fetched) fetch(nb + t); // prefetch the next batch while this one is blended
         const int cnt = min(kB16, L - base);
         if (!__any_sync(0xffffffffu, live)) continue;
         for (int g = 0; g < kB16 / 32; ++g) {
@@ -823,6 +836,7 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     finish(in1, lx + 1, p.flag & 2u, f2hi(p.r), f2hi(p.g), f2hi(p.b), f2hi(p.T), p.term1, p.nbl1);
     __syncthreads();
     const int nf = static_cast<int>(s_nflag);
+    if (nf > 0 && ranked < L) sort_all(); // the replay walks the list to the exact termination
     for (int k = warp; k < nf; k += 4)
         replay_pixel<MODE, COUNT>(A, list, L, s_flag[k], px0, py0, ev, bl);
     if (COUNT) {

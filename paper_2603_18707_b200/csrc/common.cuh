@@ -134,6 +134,7 @@ struct FrameParams {
     double campos[3];       // Camera::position() (projection.hpp:29), computed on the host
     double root_slack;      // polynomial blend kernels: the reference's alpha64 rounding near eps in
                             // q units (host_root_slack); 0 for exp
+    int sort_prefix;        // 16x16 blend: list positions its prologue ranks exactly (>= 128; INT_MAX: all)
 };
 
 #define PS_CUDA_TRY(expr)                                                  \

@@ -424,6 +424,10 @@ int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode m
     P.sh_floats4 = (sh_floats + 3) / 4;
     P.threshold_mode = host_kernel_threshold_mode(cfg.kernel);
     P.root_slack = host_root_slack(cfg.kernel);
+    // The 16x16 blend ranks only the first positions of a tile's list in its
+    // prologue (tiles terminate after ~200 entries at C2) unless the last frame
+    // replayed many pixels: a tile with a replayed pixel then sorts its whole list
+    P.sort_prefix = c->stats.replay_pixels * 8 < static_cast<uint64_t>(P.tiles_x) * P.tiles_y ? 256 : INT_MAX;
     P.kf.kind = cfg.kernel.kind;
     P.kf.order = cfg.kernel.order;
     for (int j = 0; j < 4; ++j) P.kf.c[j] = static_cast<float>(cfg.kernel.coeffs[j]);

@@ -52,6 +52,11 @@ struct TileSortSmem {
 
 // Returns the sorted bucket in shared memory (smem + LIST); with WRITEBACK also
 // writes it to pval[r.x, r.y). The caller synchronises before reading it.
+// Prefix mode (limit < L, no WRITEBACK): only the bins holding the first
+// `limit` positions are ranked and written, i.e. the list is exact on
+// [0, *ranked) with *ranked >= limit (the end of the bin holding position
+// limit - 1); positions beyond are undefined until a full sort. The blend's
+// tiles terminate after a few hundred entries (their lists are ~3x longer).
 // The bitonic fallback pads the bucket to a power of two n: it needs n 64-bit
 // keys over the nk / perm / dest arrays (2 CAP words) and n list slots; when
 // the padded bucket does not fit (CAP not a power of two), *unsorted is set and
@@ -61,7 +66,8 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
                                                    const uint32_t* __restrict__ pkey,
                                                    const unsigned long long* __restrict__ key,
                                                    const uint32_t* __restrict__ orig, uint32_t* smem,
-                                                   unsigned int* unsorted = nullptr) {
+                                                   unsigned int* unsorted = nullptr, int limit = 0x7fffffff,
+                                                   int* ranked = nullptr) {
     using S = TileSortSmem<THREADS, ROUNDS>;
     constexpr int CAP = S::CAP, BINS = S::BINS, WARPS = S::WARPS, SH = S::BIN_SHIFT;
     constexpr int PER = BINS / THREADS;
@@ -126,11 +132,26 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
 #pragma unroll
         for (int q = 0; q < PER; ++q) { hist[t * PER + q] = base; base += loc[q]; }
     }
+    // prefix mode: the ranked range ends with the bin holding position limit - 1
+    // (hist is still exclusive here: the last bin starting before `limit`)
+    int Lr = L;
+    if (limit < L) {
+        __shared__ int s_lr;
+        if (t == 0) s_lr = L;
+        __syncthreads();
+        for (int b = t; b < BINS; b += THREADS) {
+            const int s0 = static_cast<int>(hist[b]);
+            const int e0 = b + 1 < BINS ? static_cast<int>(hist[b + 1]) : L;
+            if (s0 < limit && e0 >= limit && e0 > s0) atomicMin(&s_lr, e0);
+        }
+        __syncthreads();
+        Lr = s_lr;
+    }
     __syncthreads();
     for (int j = t; j < L; j += THREADS) perm[atomicAdd(&hist[nk[j] >> SH], 1u)] = static_cast<uint16_t>(j);
     __syncthreads();
     // hist[b] is now the end of bin b: rank every item inside its bin
-    for (int p = t; p < L; p += THREADS) {
+    for (int p = t; p < Lr; p += THREADS) {
         const uint32_t j = perm[p];
         const uint32_t x = nk[j];
         const uint32_t b = x >> SH;
@@ -160,9 +181,17 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         // (only the blend prologue's CAP 1536 gets here; it passes `unsorted`)
         for (int j = t; j < L; j += THREADS) list[j] = vin[j];
         if (t == 0 && unsorted) atomicExch(unsorted, 1u);
-    } else if (!need_bitonic) {
+        Lr = L;
+    } else if (!need_bitonic && Lr == L) {
         for (int j = t; j < L; j += THREADS) list[dest[j]] = vin[j]; // coalesced read of the bucket
+    } else if (!need_bitonic) {
+        // prefix: the items of the ranked bins sit at perm positions [0, Lr)
+        for (int p = t; p < Lr; p += THREADS) {
+            const uint32_t j = perm[p];
+            list[dest[j]] = vin[j];
+        }
     } else {
+        Lr = L;
         // degenerate depth clusters: exact bitonic sort on (bits, original index);
         // full keys over the (now dead) nk / perm / dest arrays
         for (int j = t; j < L; j += THREADS) list[j] = vin[j];
@@ -194,6 +223,7 @@ __device__ __forceinline__ uint32_t* sort_one_tile(const uint2 r, uint32_t* __re
         __syncthreads();
         for (int p = t; p < L; p += THREADS) pval[r.x + p] = list[p];
     }
+    if (ranked) *ranked = Lr;
     return list;
 }
 

@@ -64,12 +64,13 @@ def ulp_diff(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.abs(ai - bi)
 
 
-def crowded_scene(n: int, seed: int, same_depth: bool = False):
+def crowded_scene(n: int, seed: int, same_depth: bool = False, opacity=(0.3, 0.95)):
     """n small splats crowded into one 16x16 tile (pixels 32-47) of a 64x64 view
     (identity camera rotation, so depth == mean z exactly): per-tile buckets of
     ~n entries exercise the long-bucket sort kernels and the global fallback;
     same_depth puts every splat at z = 5 (all sort keys equal: the tie order by
-    splat index and the bitonic path)."""
+    splat index and the bitonic path); a low `opacity` range keeps pixels live
+    deep into the list (the blend sorts past its ranked prefix)."""
     rng = np.random.default_rng(seed)
     sp = np.zeros((n, 59), dtype=np.float64)
     z = np.full(n, 5.0) if same_depth else rng.uniform(4.0, 6.0, n)
@@ -79,7 +80,7 @@ def crowded_scene(n: int, seed: int, same_depth: bool = False):
     sp[:, 3:6] = rng.uniform(0.004, 0.02, (n, 3))
     q = rng.normal(size=(n, 4))
     sp[:, 6:10] = q / np.linalg.norm(q, axis=1, keepdims=True)
-    sp[:, 10] = rng.uniform(0.3, 0.95, n)
+    sp[:, 10] = rng.uniform(opacity[0], opacity[1], n)
     sp[:, 11:14] = rng.uniform(-1.0, 1.0, (n, 3))  # SH DC (degree 0)
     cam = api.Camera(0, 64, 64, 64.0, 64.0, 32.0, 32.0, np.eye(3), np.zeros(3))
     return sp, 0, cam

@@ -37,3 +37,26 @@ def test_crowded_tiles(gpu, reference, n, seed, same, label, kname, mode):
         assert max_abs(fb.rgb, rgb_r) <= 1e-5
         assert max_abs(fb.transmittance, t_r) <= 1e-5
     ds.close()
+
+
+LOW = [(700, 21, False), (1300, 22, False), (1000, 23, True), (1500, 24, False)]
+
+
+@pytest.mark.parametrize("n,seed,same", LOW, ids=[f"n{c[0]}{'-eqz' if c[2] else ''}" for c in LOW])
+@pytest.mark.parametrize("label,kname,mode", CELLS, ids=[c[0] for c in CELLS])
+def test_crowded_low_opacity(gpu, reference, n, seed, same, label, kname, mode):
+    """Low opacities: pixels stay live past the first kSortPrefix (256) entries
+    of the crowded tile's list, so the blend ranks the rest of the bucket
+    mid-walk (blend.cu sort_all) — and before the exact replay."""
+    splats, deg, cam = crowded_scene(n, seed, same, opacity=(0.04, 0.12))
+    cfg = config(kname, mode, deg)
+    rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+    assert ctr_r["kernel_evaluations"] > 300 * 256  # pixels walk past the ranked prefix
+    ds = gpu.upload_splat3d(splats)
+    for counters in (True, False, True):
+        fb, ctr = gpu.render(ds, cam, cfg, counters=counters)
+        if counters:
+            assert ctr.as_dict() == ctr_r
+        assert max_abs(fb.rgb, rgb_r) <= 1e-5
+        assert max_abs(fb.transmittance, t_r) <= 1e-5
+    ds.close()
