@@ -145,7 +145,7 @@ typedef struct ps_stats {
     uint64_t exact_alpha_evals;/* fragments whose alpha<eps decision was re-decided in fp64 */
     float stage_ms[PS_STAGE_COUNT];
     int32_t kernel_launches;   /* kernels launched by the last call */
-    int32_t reserved;
+    int32_t sort_prefix;       /* 16x16 blend: list positions its prologue sorts next frame (INT32_MAX: all) */
 } ps_stats;
 
 typedef struct ps_ctx ps_ctx;

@@ -105,7 +105,7 @@ class ps_image_metrics(C.Structure):
         ("ssim", C.c_double),
         ("max_abs_diff", C.c_double),
         ("ssim_valid", C.c_int32),
-        ("reserved", C.c_int32),
+        ("sort_prefix", C.c_int32),
     ]
 
 
@@ -130,7 +130,7 @@ class ps_stats(C.Structure):
         ("exact_alpha_evals", C.c_uint64),
         ("stage_ms", C.c_float * 7),
         ("kernel_launches", C.c_int32),
-        ("reserved", C.c_int32),
+        ("sort_prefix", C.c_int32),
     ]
 
 

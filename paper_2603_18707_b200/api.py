@@ -627,6 +627,7 @@ class Rasterizer:
         _check(lib().ps_last_stats(self.handle, C.byref(s)), self.handle)
         return {"visible": s.visible, "pairs": s.pairs, "replay_pixels": s.replay_pixels,
                 "exact_alpha_evals": s.exact_alpha_evals, "kernel_launches": s.kernel_launches,
+                "sort_prefix": s.sort_prefix,
                 "stage_ms": {name: float(s.stage_ms[i]) for i, name in enumerate(abi.STAGES)}}
 
     def synchronize(self) -> None:
@@ -681,6 +682,11 @@ class CompareReport:
     counters_a: PerfCounters
     counters_b: PerfCounters
     pair_ratio: float
+    # device frame times (ms, median of timed frames; ablation_grid fills them):
+    # config a (the exp / StopThePop reference cell) and config b, and b's blend stage
+    frame_ms_a: Optional[float] = None
+    frame_ms_b: Optional[float] = None
+    blend_ms_b: Optional[float] = None
 
     @property
     def psnr_db(self) -> float:
@@ -727,10 +733,34 @@ ABLATION_CELLS = (
 )
 
 
+def frame_times(rasterizer: "Rasterizer", scene, cam: Camera, cfg: RasterConfig, frames: int = 5) -> dict:
+    """Device time of one frame (ms; median over `frames` frames after one
+    warm-up, stage events on the rasterizer's stream, counters off) and its
+    stage split."""
+    ds, tmp = rasterizer._scene(scene)
+    try:
+        rasterizer.render(ds, cam, cfg, counters=False)
+        rasterizer.set_timing(True)
+        runs = []
+        for _ in range(max(1, frames)):
+            rasterizer.render(ds, cam, cfg, counters=False)
+            runs.append(rasterizer.stats()["stage_ms"])
+        rasterizer.set_timing(False)
+        order = sorted(range(len(runs)), key=lambda k: sum(runs[k].values()))
+        med = runs[order[len(runs) // 2]]
+        return {"frame_ms": sum(med.values()), "stage_ms": med}
+    finally:
+        if tmp:
+            ds.close()
+
+
 def ablation_grid(rasterizer: "Rasterizer", scene, cam: Camera, base: Optional[RasterConfig] = None,
-                  background=(1.0, 1.0, 1.0), cells=ABLATION_CELLS):
+                  background=(1.0, 1.0, 1.0), cells=ABLATION_CELLS, time_frames: int = 5):
     """The reference's ablation grid (tools/main.cpp:300-345) on the device:
-    every cell compared against exp / StopThePop with the fitted kernels.
+    every cell compared against exp / StopThePop with the fitted kernels, and
+    (time_frames > 0) each cell's device frame time (the paper's Table 3 with
+    measured times instead of pair counts): frame_ms_b /
+    blend_ms_b of every report, frame_ms_a = the exp / StopThePop frame.
     Returns (reports by label, csv text in the reference's format)."""
     base = base or RasterConfig()
     ds, tmp = rasterizer._scene(scene)
@@ -741,9 +771,16 @@ def ablation_grid(rasterizer: "Rasterizer", scene, cam: Camera, base: Optional[R
                                 kernel=fitted_kernel(kname), v_dilation=base.v_dilation,
                                 sh_degree=base.sh_degree, clamp_before_blend=base.clamp_before_blend)
         ref = cfg("exp", CullingMode.StopThePop)
+        ref_t = frame_times(rasterizer, ds, cam, ref, time_frames) if time_frames > 0 else None
         reports, csv = {}, csv_header()
         for label, kname, mode in cells:
-            r = rasterizer.compare(ds, cam, ref, cfg(kname, mode), background)
+            c = cfg(kname, mode)
+            r = rasterizer.compare(ds, cam, ref, c, background)
+            if ref_t is not None:
+                t = frame_times(rasterizer, ds, cam, c, time_frames)
+                r.frame_ms_a = ref_t["frame_ms"]
+                r.frame_ms_b = t["frame_ms"]
+                r.blend_ms_b = t["stage_ms"].get("blend")
             reports[label] = r
             csv += csv_row("exp/stp", label, r)
         return reports, csv

@@ -737,9 +737,11 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     };
     fetch(t); // the ranked prefix holds at least the first batch
     bool fetched = true;
+    int staged = 0; // list positions staged (the tile's walk ended before them)
     for (int base = 0; base < L; base += kB16) {
         const bool live = (f2lo(p.x) == f2lo(p.x)) || (f2hi(p.x) == f2hi(p.x));
         if (__syncthreads_count(live) == 0) break;
+        staged = base + kB16;
         if (!fetched) { // this batch lies beyond the sorted prefix (rare)
             sort_all();
             fetch(base + t);
@@ -837,6 +839,12 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
     __syncthreads();
     const int nf = static_cast<int>(s_nflag);
     if (nf > 0 && ranked < L) sort_all(); // the replay walks the list to the exact termination
+    if (sort_here && t == 0) { // how far down its list this tile needed the exact order
+        const int need = nf > 0 ? L : min(L, staged);
+        if (need > 256) atomicAdd(&A.ctr->need_over[0], 1u);
+        if (need > 512) atomicAdd(&A.ctr->need_over[1], 1u);
+        if (need > 1024) atomicAdd(&A.ctr->need_over[2], 1u);
+    }
     for (int k = warp; k < nf; k += 4)
         replay_pixel<MODE, COUNT>(A, list, L, s_flag[k], px0, py0, ev, bl);
     if (COUNT) {

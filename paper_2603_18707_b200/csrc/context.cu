@@ -162,6 +162,8 @@ struct ps_ctx {
     int64_t p_cap = 0;
     uint32_t last_max_len = 0; // longest bucket of the last rendered frame (speculation hint)
     int64_t clean_tiles = 0;   // the last frame's blend left the counters and this many tile counts zero
+    int sort_prefix = 256;      // blend prologue sort prefix for the next frame (adapt_sort_prefix)
+    int64_t frame_tiles = 0;    // tiles of the frame in flight
     int64_t pix_cap = 0;
     int64_t tiles_cap = 0;
     FrameDev f;
@@ -427,7 +429,11 @@ int make_params(ps_ctx* c, const ps_camera& cam, const ps_config& cfg_in, Mode m
     // The 16x16 blend ranks only the first positions of a tile's list in its
     // prologue (tiles terminate after ~200 entries at C2) unless the last frame
     // replayed many pixels: a tile with a replayed pixel then sorts its whole list
-    P.sort_prefix = c->stats.replay_pixels * 8 < static_cast<uint64_t>(P.tiles_x) * P.tiles_y ? 256 : INT_MAX;
+    P.sort_prefix = c->sort_prefix;
+    c->frame_tiles = static_cast<int64_t>(P.tiles_x) * P.tiles_y;
+#ifdef PS_AB_FULLSORT
+    P.sort_prefix = INT_MAX;
+#endif
     P.kf.kind = cfg.kernel.kind;
     P.kf.order = cfg.kernel.order;
     for (int j = 0; j < 4; ++j) P.kf.c[j] = static_cast<float>(cfg.kernel.coeffs[j]);
@@ -475,12 +481,29 @@ int check_frame_counters(ps_ctx* c, const ps_scene* s, FrameResult& res) {
     return PS_OK;
 }
 
+// The 16x16 blend ranks only the first sort_prefix positions of a tile's list
+// in its prologue and the rest when the walk (or the exact replay) gets there,
+// which costs a second sort. Tiles terminate after a scene-dependent depth
+// (C2: ~200 entries; C4 / C5 deeper), so each frame reports how many tiles
+// needed more than 256 / 512 / 1024 positions, and the next frame of this
+// context uses the smallest prefix at most 1/5 of the tiles outgrew (whole
+// lists otherwise; measured at C2-C5: 256 at C2 / C3, 512 at C4 / C5, whole
+// lists for exp and poly3, whose replayed pixels need whole lists). Results do not depend on it (the order is exact either way).
+void adapt_sort_prefix(ps_ctx* c, const FrameResult& res) {
+    const uint64_t nt = static_cast<uint64_t>(c->frame_tiles);
+    if (nt == 0) return;
+    const uint32_t* over = res.ctr.need_over;
+    c->sort_prefix = over[0] * 5 <= nt ? 256 : over[1] * 5 <= nt ? 512 : over[2] * 5 <= nt ? 1024 : INT_MAX;
+}
+
 void frame_stats(ps_ctx* c, const FrameResult& res) {
+    adapt_sort_prefix(c, res);
     c->stats.visible = res.visible;
     c->stats.pairs = res.pairs;
     c->stats.replay_pixels = res.ctr.replay_px;
     c->stats.exact_alpha_evals = res.ctr.exact_evals;
     c->stats.kernel_launches = res.launches;
+    c->stats.sort_prefix = c->sort_prefix;
     if (c->timing) {
         for (int k = 0; k < PS_STAGE_COUNT; ++k) {
             float ms = 0.f;
@@ -514,7 +537,7 @@ int finish_frame(ps_ctx* c, const ps_scene* s, const ps_camera& cam, const ps_co
         return run_frame(c, s, cam, cfg_in, sized, res);
     }
     frame_stats(c, res);
-    // K7's last CTA zeroed the counters, the blend's CTAs the frame's tile counts
+    // the blend's last CTA zeroed the counters, its CTAs the frame's tile counts
     const int64_t ts = cfg_in.tile_size;
     c->clean_tiles = res.published ? ((cam.width + ts - 1) / ts) * ((cam.height + ts - 1) / ts) : 0;
     return PS_OK;

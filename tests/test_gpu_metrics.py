@@ -112,3 +112,7 @@ def test_ablation_grid_counts_match_reference(gpu, reference, c1):
         assert reports[label].counters_b.tile_pairs_after_tight_test == want["tile_pairs_after_tight_test"]
     # the reference row compared with itself
     assert reports["exp/stp"].psnr_db == math.inf and reports["exp/stp"].pair_ratio == 1.0
+    # measured device times for every cell (the paper's Table 3 with times)
+    for label, _, _ in api.ABLATION_CELLS:
+        r = reports[label]
+        assert r.frame_ms_a > 0.0 and r.frame_ms_b > 0.0 and 0.0 < r.blend_ms_b <= r.frame_ms_b
