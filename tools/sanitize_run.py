@@ -1,8 +1,10 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): C1 (G(10k, seed 1), 256x256) through every blend variant the
 bench and tests use — poly1 / exp / poly3 / a non-monotone kernel, 16x16 and
-8x8 tiles, a sized then a speculative frame, a view batch, a crowded tile with
-equal depths, and the device metrics."""
+8x8 and 48x48 tiles, a sized then a speculative frame, counter-free frames, a
+view batch, a crowded tile with equal depths, low-opacity crowded tiles (the
+blend's prefix sort completed mid-walk and before the replay), the TMA-staged
+K1, and the device metrics."""
 import os
 import sys
 
@@ -32,5 +34,14 @@ with api.Rasterizer(0) as r:
     cs, cdeg, ccam = crowded_scene(1300, 16, True)
     r.render(cs, ccam, cfg)
     r.render(cs, ccam, cfg)
+    # low opacities: the blend sorts past its ranked prefix mid-walk / before the replay
+    ls, ldeg, lcam = crowded_scene(700, 21, False, opacity=(0.04, 0.12))
+    for kname, mode in (("poly1", api.CullingMode.OpacityAware), ("exp", api.CullingMode.StopThePop)):
+        lc = api.RasterConfig(kernel=api.fitted_kernel(kname), culling_mode=mode, sh_degree=ldeg)
+        r.render(ls, lcam, lc)
+        r.render(ls, lcam, lc, counters=False)
+    r.render(ds, cams[1], cfg, counters=False)  # the counter-free blend the bench times
+    r.render(ds, cams[1], api.RasterConfig(kernel=api.fitted_kernel("poly1"), culling_mode=api.CullingMode.OpacityAware,
+                                           sh_degree=deg, tile_size=48))
     ds.close()
 print("sanitize workload done")
