@@ -853,56 +853,24 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
 // the same thread, so the HBM-bound SH traffic overlaps the fp64-latency-bound
 // geometry of other warps, and the conic / opacity stay in registers.
 // MINB: CTAs per SM the registers are budgeted for (3 at <= 1.5M splats, 2 above)
-// The CTA's SH coefficients (sh_floats4 plane-major float4 planes, 4 KB of
-// each for 256 splats: most of K1's HBM traffic) are requested at kernel entry
-// by TMA bulk copies into shared memory, so the stream runs under the fp64
-// geometry and the shading reads shared memory (K1_TMA_SH; dynamic smem
-// sh_floats4 x 4 KB).
 template <int BC, int BK, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
-    extern __shared__ __align__(128) float4 s_sh[]; // [sh_floats4][256]
-    __shared__ __align__(8) unsigned long long s_bar;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
-    const int64_t i = i0 + threadIdx.x;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = i < s.n;
-    const int nf4 = P.sh_floats4;
-    auto issue = [&]() {
-        const unsigned cnt = static_cast<unsigned>(min(static_cast<int64_t>(blockDim.x), s.n - i0));
-        mbar_arrive_expect_tx(&s_bar, cnt * 16u * static_cast<unsigned>(nf4));
-        for (int j = 0; j < nf4; ++j)
-            bulk_copy_g2s(s_sh + j * blockDim.x, s.sh4 + j * s.n + i0, cnt * 16u, &s_bar);
-    };
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-#ifndef PS_K1_TMA_LATE
-        issue();
-#endif
-    }
     double mean[3] = {0.0, 0.0, 0.0}, c6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, opacity = 0.0;
     if (in) {
         for (int k = 0; k < 3; ++k) mean[k] = s.mean[k][i];
         for (int k = 0; k < 6; ++k) c6[k] = s.cov[k][i];
         opacity = s.opacity[i];
     }
-    __syncthreads(); // the barrier's initialisation precedes every wait
     GeoOut g;
-#ifdef PS_K1_TMA_LATE
-    if (threadIdx.x == 0) issue();
-#endif
     geometry_view<BC>(i, in, mean, c6, opacity, P, f, ctr, &g);
     pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
     if (g.visible) {
-        mbar_wait(&s_bar, 0);
         float v[48];
-#pragma unroll
-        for (int j = 0; j < kShPlanes; ++j) {
-            const float4 t = j < nf4 ? s_sh[j * blockDim.x + threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
-            v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
-        }
+        load_sh<1>(s, i, P.sh_floats4, v);
         const bool same = kThresholdIsBound<BC, BK> && !P.cfg.has_culling_kernel;
         shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o, same ? &g.x : nullptr);
-    } else if (threadIdx.x == 0) {
-        mbar_wait(&s_bar, 0); // no exit while the copies are in flight
     }
 }
 
@@ -1255,17 +1223,9 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
     // 1,004 us at 2 CTAs per SM, although back-to-back unflushed frames show it
     // 5% ahead)
     constexpr int64_t kFusedMax = 1500000;
-    const size_t sh_smem = static_cast<size_t>(P.sh_floats4) * 256 * sizeof(float4);
 #define PS_FUSED(BCV, BKV)                                                                 \
     if (s.n <= kFusedMax && P.bound_class == BCV && P.blend_class == BKV) {              \
-        static bool attr = false;                                                        \
-        if (!attr) {                                                                     \
-            cudaFuncSetAttribute(k_preprocess<BCV, BKV, 3>,                              \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,            \
-                                 kShPlanes * 256 * static_cast<int>(sizeof(float4)));    \
-            attr = true;                                                                 \
-        }                                                                                \
-        k_preprocess<BCV, BKV, 3><<<blocks, 256, sh_smem, st>>>(s, P, f, ctr);           \
+        k_preprocess<BCV, BKV, 3><<<blocks, 256, 0, st>>>(s, P, f, ctr);                 \
         return 1;                                                                        \
     }
     PS_FUSED(kBcStp, kBkExp)
