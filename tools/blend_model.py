@@ -100,7 +100,15 @@ for t in range(0, tx_n * ty_n, step):
     per_g = pcg.reshape(ng, 32, 16, 8).sum(axis=1)       # [ng, 16, 8]
     gmax = sum(int(per_g[:, (w >> 1) * 8:(w >> 1) * 8 + 8, (w & 1) * 4:(w & 1) * 4 + 4].reshape(ng, -1).max(axis=1).sum())
                for w in range(4))
-    group_stats.append(gmax)
+    gm2 = []
+    for G in (64, 128):
+        ngG = (L + G - 1) // G
+        pcG = np.zeros((ngG * G, 16, 8), bool)
+        pcG[:L] = pc
+        perG = pcG.reshape(ngG, G, 16, 8).sum(axis=1)
+        gm2.append(sum(int(perG[:, (w >> 1) * 8:(w >> 1) * 8 + 8, (w & 1) * 4:(w & 1) * 4 + 4].reshape(ngG, -1).max(axis=1).sum())
+                       for w in range(4)))
+    group_stats.append((gmax, gm2[0], gm2[1]))
     evals = np.where(inside, np.minimum(term + 1, L), 0).sum()
     blended = (acc & live & inside[None, :]).sum()
     last = int(np.where(inside, np.minimum(term + 1, L), 0).max())   # entries the tile needs
@@ -135,7 +143,8 @@ print(f"warp walk steps (max over lanes) {wmax.sum()}  lane-steps {wsum.sum()}  
 print(f"per tile: L mean {L.mean():.0f} p50 {np.median(L):.0f} p99 {np.percentile(L, 99):.0f} max {L.max()}; "
       f"warp max steps per tile (max over warps): p50 {np.median(wmax.max(1)):.0f} max {wmax.max()}")
 gm = np.array(group_stats)
-print(f"warp walk steps with the SIMT max taken per 32-record group: {gm.sum()} (SIMT {wsum.sum() / (32 * gm.sum()):.3f})")
+for k, G in enumerate((32, 64, 128)):
+    print(f"warp walk steps with the SIMT max taken per {G}-record group: {gm[:, k].sum()} (SIMT {wsum.sum() / (32 * gm[:, k].sum()):.3f})")
 qs_ = np.array(quad_stats)
 print(f"1x4 quad steps {qs_[:, 0].sum()} (x{qs_[:, 0].sum() * 4 / cand.sum():.3f} slots/cand), warp max-steps {qs_[:, 1].sum()} "
       f"(2 warps/tile, SIMT {qs_[:, 0].sum() / (32 * qs_[:, 1].sum()):.3f})")
