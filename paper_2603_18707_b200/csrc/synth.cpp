@@ -197,12 +197,11 @@ int ps_synth_scene_soa(int kind, uint64_t seed, int64_t n, double* means, double
         ps::g_free_error = "unknown synthetic scene kind or size";
         return PS_INVALID_ARGUMENT;
     }
-    // generate in chunks of AoS records to bound the temporary
+    // the generator draws the whole scene in the reference's order (one
+    // mt19937_64 stream), into a full AoS temporary (472 B per splat)
     int deg = 0;
-    const int64_t chunk = std::min<int64_t>(count, 1 << 16);
     std::vector<double> tmp(static_cast<size_t>(PS_SPLAT3D_DOUBLES) * count);
     generate(kind, seed, count, tmp.data(), &deg);
-    (void)chunk;
     for (int64_t i = 0; i < count; ++i) {
         const double* p = tmp.data() + i * PS_SPLAT3D_DOUBLES;
         for (int k = 0; k < 3; ++k) means[3 * i + k] = p[k];
