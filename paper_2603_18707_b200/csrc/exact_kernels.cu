@@ -609,7 +609,9 @@ struct GeoOut {
     double x = 0.0;                             // the culling root (bound_for)
 };
 
-template <int BC>
+// CTA_RED: the frame counters are reduced over the CTA before their atomics
+// (one update per CTA instead of per warp; see the end).
+template <int BC, bool CTA_RED = false>
 __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
                                               double opacity, const FrameParams& P, const FrameDev& f,
                                               DevCounters* ctr, GeoOut* out = nullptr) {
@@ -744,15 +746,43 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
     coarse = warp_sum_u64(coarse);
     tight = warp_sum_u64(tight);
     visible = warp_sum_u64(visible);
-    if ((threadIdx.x & 31) == 0) {
-        if (kmax) {
-            atomicMax(&ctr->key_min, kmin_inv);
-            atomicMax(&ctr->key_max, kmax);
+    if (!CTA_RED) {
+        if ((threadIdx.x & 31) == 0) {
+            if (kmax) {
+                atomicMax(&ctr->key_min, kmin_inv);
+                atomicMax(&ctr->key_max, kmax);
+            }
+            if (frustum) atomicAdd(&ctr->frustum, frustum);
+            if (coarse) atomicAdd(&ctr->coarse, coarse);
+            if (tight) atomicAdd(&ctr->tight, tight);
+            if (visible) atomicAdd(&ctr->visible, visible);
         }
-        if (frustum) atomicAdd(&ctr->frustum, frustum);
-        if (coarse) atomicAdd(&ctr->coarse, coarse);
-        if (tight) atomicAdd(&ctr->tight, tight);
-        if (visible) atomicAdd(&ctr->visible, visible);
+        return;
+    }
+    // one set of counter atomics per CTA: the six counter words are single L2
+    // addresses every CTA of the grid updates, and per warp (3-6M splats: up to
+    // ~190k updates per address per frame) they throttled the fused K1 at scale
+    // (C3 preprocess 1,437 -> 870 us, C4 707 -> 405 us with this; at 1M the
+    // per-warp atomics are as fast and the split kernels slower with it)
+    __shared__ unsigned long long s_red[6][8];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_red[0][w] = kmin_inv; s_red[1][w] = kmax; s_red[2][w] = frustum;
+        s_red[3][w] = coarse; s_red[4][w] = tight; s_red[5][w] = visible;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        unsigned long long v = s_red[k][0];
+        for (int j = 1; j < nw; ++j) v = k < 2 ? max(v, s_red[k][j]) : v + s_red[k][j];
+        if (v) {
+            if (k == 0) atomicMax(&ctr->key_min, v);
+            else if (k == 1) atomicMax(&ctr->key_max, v);
+            else if (k == 2) atomicAdd(&ctr->frustum, v);
+            else if (k == 3) atomicAdd(&ctr->coarse, v);
+            else if (k == 4) atomicAdd(&ctr->tight, v);
+            else atomicAdd(&ctr->visible, v);
+        }
     }
 }
 
@@ -852,8 +882,9 @@ __global__ void __launch_bounds__(256) k_shade(SceneDev s, FrameParams P, FrameD
 // pairs): the SH loads and colour of a visible splat follow its projection in
 // the same thread, so the HBM-bound SH traffic overlaps the fp64-latency-bound
 // geometry of other warps, and the conic / opacity stay in registers.
-// MINB: CTAs per SM the registers are budgeted for (3 at <= 1.5M splats, 2 above)
-template <int BC, int BK, int MINB>
+// MINB: CTAs per SM the registers are budgeted for; CTA_RED: counters reduced
+// per CTA (above kFusedWarpCounters splats)
+template <int BC, int BK, int MINB, bool CTA_RED>
 __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParams P, FrameDev f, DevCounters* ctr) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = i < s.n;
@@ -864,7 +895,7 @@ __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParam
         opacity = s.opacity[i];
     }
     GeoOut g;
-    geometry_view<BC>(i, in, mean, c6, opacity, P, f, ctr, &g);
+    geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g);
     pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
     if (g.visible) {
         float v[48];
@@ -1217,15 +1248,18 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
     if (s.n == 0) return 0;
     const int blocks = static_cast<int>((s.n + 255) / 256);
     // fused K1 for the fitted-kernel cells of the reference's grid (main.cpp:315-323)
-    // up to 1.5M splats (3 CTAs per SM, 80 registers): at 1M 162 us against 191
-    // at 2 CTAs and 201 split. Above, the split K1a / K1b: in the bench's
-    // L2-flushed frames the fused kernel loses there (C3 preprocess 1,337 vs
-    // 1,004 us at 2 CTAs per SM, although back-to-back unflushed frames show it
-    // 5% ahead)
-    constexpr int64_t kFusedMax = 1500000;
+    // (3 CTAs per SM, 80 registers): at 1M 162 us against 191 at 2 CTAs and 201
+    // for the split K1a / K1b below. Above 1.5M splats its frame counters are
+    // reduced per CTA (geometry_view CTA_RED): with per-warp counter atomics the
+    // fused kernel lost to the split ones at scale (C3 1,437 vs 1,027 us),
+    // with per-CTA ones it wins there too (870 us)
+    constexpr int64_t kFusedWarpCounters = 1500000;
 #define PS_FUSED(BCV, BKV)                                                                 \
-    if (s.n <= kFusedMax && P.bound_class == BCV && P.blend_class == BKV) {              \
-        k_preprocess<BCV, BKV, 3><<<blocks, 256, 0, st>>>(s, P, f, ctr);                 \
+    if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
+        if (s.n <= kFusedWarpCounters)                                                   \
+            k_preprocess<BCV, BKV, 3, false><<<blocks, 256, 0, st>>>(s, P, f, ctr);      \
+        else                                                                             \
+            k_preprocess<BCV, BKV, 3, true><<<blocks, 256, 0, st>>>(s, P, f, ctr);       \
         return 1;                                                                        \
     }
     PS_FUSED(kBcStp, kBkExp)
