@@ -197,11 +197,20 @@ class Ours:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # PS_BENCH_DEVICE / PS_BENCH_BACKEND=gloo: dry runs of the N > 1 path with
+        # every rank on one GPU (tools/runs/r02_bench_n2_dryrun.sh); the driver's
+        # runs use one GPU per rank and NCCL
+        if os.environ.get("PS_BENCH_DEVICE"):
+            self.local = int(os.environ["PS_BENCH_DEVICE"])
+        self.backend = os.environ.get("PS_BENCH_BACKEND", "nccl")
         torch.cuda.set_device(self.local)
         self.dist = None
         if self.world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
             self.dist = dist
         self.lib = api.lib()
         self.r = api.Rasterizer(self.local)
@@ -215,7 +224,7 @@ class Ours:
 
     def max_ms(self, ms: float) -> float:
         from paper_2603_18707_b200.sharding import max_over_ranks
-        return max_over_ranks(ms, self.dist, device="cuda")
+        return max_over_ranks(ms, self.dist, device="cuda" if self.backend == "nccl" else "cpu")
 
     def cfg(self, kname: str, mode: str, deg: int):
         api = self.api
