@@ -483,17 +483,27 @@ int check_frame_counters(ps_ctx* c, const ps_scene* s, FrameResult& res) {
 
 // The 16x16 blend ranks only the first sort_prefix positions of a tile's list
 // in its prologue and the rest when the walk (or the exact replay) gets there,
-// which costs a second sort. Tiles terminate after a scene-dependent depth
-// (C2: ~200 entries; C4 / C5 deeper), so each frame reports how many tiles
-// needed more than 256 / 512 / 1024 positions, and the next frame of this
-// context uses the smallest prefix at most 1/5 of the tiles outgrew (whole
-// lists otherwise; measured at C2-C5: 256 at C2 / C3, 512 at C4 / C5, whole
-// lists for exp and poly3, whose replayed pixels need whole lists). Results do not depend on it (the order is exact either way).
+// which costs a second, whole sort. Tiles terminate after a scene-dependent
+// depth (C2: ~200 entries; C4 / C5 deeper) and a tile with a replayed pixel
+// needs its whole list, so each frame reports how many tiles needed more than
+// 256 / 512 / 1024 positions, and the next frame of this context takes the
+// prefix of least modelled sort cost: a sort's fixed half (keys, histogram,
+// scan, bin scatter over the whole bucket) plus its ranking half in proportion
+// to the positions ranked, plus one whole sort for every tile that outgrows the
+// prefix; whole lists cost 1. Measured choices: 256 at C2 / C3, 512 at C4,
+// whole lists for C5, exp and poly3. Results do not depend on it.
 void adapt_sort_prefix(ps_ctx* c, const FrameResult& res) {
-    const uint64_t nt = static_cast<uint64_t>(c->frame_tiles);
-    if (nt == 0) return;
-    const uint32_t* over = res.ctr.need_over;
-    c->sort_prefix = over[0] * 5 <= nt ? 256 : over[1] * 5 <= nt ? 512 : over[2] * 5 <= nt ? 1024 : INT_MAX;
+    const double nt = static_cast<double>(c->frame_tiles);
+    if (!(nt > 0.0)) return;
+    const double lavg = std::max(1.0, static_cast<double>(res.pairs) / nt);
+    const int prefixes[3] = {256, 512, 1024};
+    int best = INT_MAX;
+    double best_cost = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        const double cost = 0.5 + 0.5 * std::min(1.0, prefixes[k] / lavg) + res.ctr.need_over[k] / nt;
+        if (cost < best_cost) { best_cost = cost; best = prefixes[k]; }
+    }
+    c->sort_prefix = best;
 }
 
 void frame_stats(ps_ctx* c, const FrameResult& res) {

@@ -202,7 +202,12 @@ __device__ void blend_record(double a, double b, double c, double o, const Frame
                 kmag += fabs(k.coeffs[j]) * qp;
                 qp *= qb;
             }
-            kmag *= 2.0 * k.order + 2.0; // folded o*c_j products + Horner FFMAs
+            // Horner with FMA rounds once per step, so the term a_j q^j carries
+            // at most j (<= order) roundings (Higham, Accuracy and Stability,
+            // 5.1), plus one for the folded coefficient o c_j in fp32 (quadric
+            // mode) or for the fp32 coefficient and the final o * p (alpha
+            // mode): gamma_{order+2} sum |c_j| q^j, with 10% slack
+            kmag *= k.order + 2.2;
         } else {
             // ex2.approx (2^-22) + fp32 rounding of its argument (|arg| <= 0.73 qb + |log2 o|)
             extra = amax * (2.4e-7 + (0.73 * qb + fabs(log2(o)) + 1.0) * e32 * 0.7);

@@ -102,7 +102,7 @@ else:
     d = [coef[1] if k.order >= 1 else 0.0, 2 * coef[2] if k.order >= 2 else 0.0, 3 * coef[3] if k.order >= 3 else 0.0]
     dp = lambda q: np.abs(d[0] + d[1] * q + d[2] * q * q)  # noqa: E731
     kp = np.maximum(dp(0.0), dp(qb))
-    kmag = sum(np.abs(coef[j]) * qb ** j for j in range(k.order + 1)) * (2.0 * k.order + 2.0)
+    kmag = sum(np.abs(coef[j]) * qb ** j for j in range(k.order + 1)) * ((2.0 * k.order + 2.0) if a.old else (k.order + 2.2))
     extra = 0.0
 Ga_terms = {"o k' Gq": 1.02 * o * kp * Gq, "eval": 1.02 * e32 * o * kmag, "exp": 1.02 * extra + 0 * o,
             "2u amax": 2.0 * e32 * amax}
