@@ -318,17 +318,25 @@ __device__ __forceinline__ F2 f2fma(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, 
 // centre) is <= q_hi is included: q_hi is inflated by the quadric's rounding
 // (~5u relative) and the half-width by the approximate rcp/sqrt error plus an
 // absolute margin; a pair included in excess only costs one skipped step.
-__device__ __forceinline__ uint32_t row_pairs(int row, float mx, float my, float beta, float gamma, float qpad,
-                                              float ia) {
-    const float dy = (row + 0.5f) - my;
-    const float rhs = fmaf(-gamma * dy, dy, qpad);
-    const float mr = fmaf(-beta, dy, mx);
-    float h = sqrt_approx(fmaxf(rhs, 0.0f) * ia);
-    h = fmaf(h, 1.00002f, fmaf(fabsf(mr), 2e-6f, 1e-3f));
-    if (!(rhs >= 0.0f)) h = -1.0f; // empty row
-    const int lo = min(max(__float2int_ru(mr - h - 0.5f), 0), 16) >> 1;
-    const int hi = max(min(__float2int_rd(mr + h - 0.5f), 15), -2) >> 1;
-    return (0xFFu << lo) & (0xFFu >> (7 - hi));
+// Rows r and r + 8 at once: the per-row floating-point work in packed f32x2
+// (C2 blend -3.7 us against one row at a time).
+__device__ __forceinline__ void row_pairs2(int row, float mx, float my, float beta, float gamma, float qpad,
+                                           float ia, uint32_t& m_lo, uint32_t& m_hi) {
+    const F2 dy = f2sub(f2(row + 0.5f, row + 8.5f), f2b(my));
+    const F2 rhs = f2fma(f2mul(f2b(-gamma), dy), dy, f2b(qpad));
+    const F2 mr = f2fma(f2b(-beta), dy, f2b(mx));
+    const F2 h2 = f2mul(f2(fmaxf(f2lo(rhs), 0.0f), fmaxf(f2hi(rhs), 0.0f)), f2b(ia));
+    F2 h = f2(sqrt_approx(f2lo(h2)), sqrt_approx(f2hi(h2)));
+    h = f2fma(h, f2b(1.00002f), f2fma(f2(fabsf(f2lo(mr)), fabsf(f2hi(mr))), f2b(2e-6f), f2b(1e-3f)));
+    const float h0 = f2lo(rhs) >= 0.0f ? f2lo(h) : -1.0f; // empty rows
+    const float h1 = f2hi(rhs) >= 0.0f ? f2hi(h) : -1.0f;
+    const F2 hh = f2(h0, h1);
+    const F2 l = f2sub(f2sub(mr, hh), f2b(0.5f));
+    const F2 r = f2sub(f2add(mr, hh), f2b(0.5f));
+    const int lo0 = min(max(__float2int_ru(f2lo(l)), 0), 16) >> 1, lo1 = min(max(__float2int_ru(f2hi(l)), 0), 16) >> 1;
+    const int hi0 = max(min(__float2int_rd(f2lo(r)), 15), -2) >> 1, hi1 = max(min(__float2int_rd(f2hi(r)), 15), -2) >> 1;
+    m_lo = (0xFFu << lo0) & (0xFFu >> (7 - hi0));
+    m_hi = (0xFFu << lo1) & (0xFFu >> (7 - hi1));
 }
 
 // Record-local split of a tile-local coordinate v (see the record layout below).
@@ -782,11 +790,14 @@ __global__ void __launch_bounds__(128, 8) k_blend16(const BlendArgs A) {
                 const float qpad = qhi * 1.000004f;
                 const float ia = rcp_approx(Aq) * 1.000002f;
 #pragma unroll
-                for (int row = 0; row < 16; ++row) {
-                    const uint32_t m8 = row_pairs(row, mx, my, beta, gamma, qpad, ia);
-                    const int wb = (row >> 3) << 1, sh = (row & 7) << 2;
-                    cw[wb] |= (m8 & 0xFu) << sh;
-                    cw[wb + 1] |= (m8 >> 4) << sh;
+                for (int row = 0; row < 8; ++row) { // rows row and row + 8 (words 0,1 and 2,3)
+                    uint32_t m0, m1;
+                    row_pairs2(row, mx, my, beta, gamma, qpad, ia, m0, m1);
+                    const int sh = row << 2;
+                    cw[0] |= (m0 & 0xFu) << sh;
+                    cw[1] |= (m0 >> 4) << sh;
+                    cw[2] |= (m1 & 0xFu) << sh;
+                    cw[3] |= (m1 >> 4) << sh;
                 }
             }
 #pragma unroll

@@ -19,7 +19,7 @@ k = find(r"__global__ void __launch_bounds__\(128, .*\) k_blend16")
 ranges = {
     "walk": (find(r"^struct Frag \{"), find(r"^// Exact replay of one flagged pixel")),
     "replay": (find(r"^// Exact replay of one flagged pixel"), find(r"^// CAPR: rounds")),
-    "cover(row_pairs)": (find(r"row_pairs\(int row"), find(r"^// Record-local split")),
+    "cover(row_pairs2)": (find(r"row_pairs2\(int row"), find(r"^// Record-local split")),
     "transpose": (find(r"warp_transpose32\(uint32_t x"), find(r"^// ---- packed fp32 pairs")),
     "blend16 prologue": (k, find(r"for \(int base = 0; base < L; base \+= kB16\)", k)),
     "batch barrier+stage": (find(r"for \(int base = 0; base < L; base \+= kB16\)", k), find(r"coverage of \{q <= q_hi\}", k)),
