@@ -86,3 +86,32 @@ def test_query_modes_interleaved_with_renders(reference):
                 rgb_r, t_r, ctr_r = reference.render(splats, cv.to_struct(), cfg.to_struct())
                 assert ctr.as_dict() == ctr_r
                 assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL
+
+
+def test_sort_prefix_adapts_across_frames(reference):
+    """The blend's prologue sort prefix is chosen per context from the previous
+    frame (context.cu adapt_sort_prefix): low-opacity crowded tiles whose walks
+    run past 256 / 512 entries grow it (whole lists), ordinary frames shrink it
+    back to 256, and kernel cells with many replayed pixels keep whole lists.
+    Every frame of the alternation stays exact against the reference."""
+    dense = crowded_scene(1300, 22, False, opacity=(0.04, 0.12))
+    plain = (*scene("g", 1, 100000), camera(1, 256, 256, 0))  # lists of up to ~2,400 entries
+    seq = [(plain, "poly1", api.CullingMode.OpacityAware), (dense, "poly1", api.CullingMode.OpacityAware),
+           (dense, "exp", api.CullingMode.StopThePop), (plain, "poly1", api.CullingMode.OpacityAware),
+           (plain, "exp", api.CullingMode.StopThePop), (plain, "poly1", api.CullingMode.OpacityAware),
+           (dense, "poly1", api.CullingMode.OpacityAware)]
+    prefixes = []
+    with api.Rasterizer(0) as r:
+        for (splats, deg, cam), kname, mode in seq:
+            cfg = config(kname, mode, deg)
+            rgb_r, t_r, ctr_r = reference.render(splats, cam.to_struct(), cfg.to_struct())
+            for counters in (True, False):
+                fb, ctr = r.render(splats, cam, cfg, counters=counters)
+                if counters:
+                    assert ctr.as_dict() == ctr_r
+                assert max_abs(fb.rgb, rgb_r) <= IMAGE_TOL
+                assert max_abs(fb.transmittance, t_r) <= IMAGE_TOL
+                prefixes.append(r.stats()["sort_prefix"])
+    # the crowded low-opacity tile (~650 entries, never terminating) outgrows
+    # the smallest prefix, so the state did change along the sequence
+    assert max(prefixes) > 256 and len(set(prefixes)) > 1, prefixes
