@@ -1,10 +1,13 @@
 // blend.cu — K6: front-to-back alpha blending per tile (raster.cpp:227-301).
 //
-// One CTA per tile, one pixel per thread (tile_size^2 <= 1024; larger tiles in
-// chunks of 1024 pixels). The tile's
-// splat list is staged through shared memory in batches of blockDim records
-// (gathered by splat index from the fp32 blend records written by K1, with the
-// fp64 mean turned into tile-local fp32 coordinates on the way in).
+// Two kernels. k_blend16 (tile_size 16, the reference default): 128 threads per
+// tile, a pixel PAIR per thread in packed f32x2, the tile's bucket sorted in
+// its prologue (only the prefix the walk needs, tile_sort.cuh), records staged
+// through shared memory in record-local fp32 coordinates with per-record
+// coverage masks, and the exact fp64 replay of flagged pixels fused at the end
+// (see the comments above k_blend16). k_blend (other tile sizes): one pixel per
+// thread, tiles above 32x32 in chunks of 1024 pixels, tile-local coordinates,
+// replay by K7 (exact_kernels.cu k_replay).
 //
 // Per (pixel, splat) the fast path is
 //     u = (dx + beta dy);  q = A u^2 + gamma dy^2;  skip unless q <= q_hi
@@ -12,11 +15,11 @@
 // quadric space: for a kernel non-increasing in q, min(.999, o k(q)) >= eps
 // <=> q <= q*(o). No MUFU on the skip path for any kernel; polynomial kernels
 // evaluate alpha with FFMA only. q in [q_lo, q_hi] (the certified fp32 error
-// band) is re-decided with the reference's fp64 arithmetic (exact_alpha_ge_eps).
-// The transmittance test (raster.cpp:272-277) carries a per-pixel absolute
-// error bound on T; a pixel whose test value lands inside that band around the
-// floor is flagged and replayed exactly in fp64 by K7. Early termination: the CTA stops
-// when no pixel is live (__syncthreads_count), the reference's `remaining == 0`.
+// band) is re-decided with the reference's fp64 arithmetic. The transmittance
+// test (raster.cpp:272-277) carries certified bounds on the reference's T; a
+// pixel whose test lands inside the band around the floor is flagged and
+// replayed exactly in fp64. Early termination: the CTA stops when no pixel is
+// live (__syncthreads_count), the reference's `remaining == 0`.
 #include <algorithm>
 
 #include "kernels.h"
