@@ -26,6 +26,8 @@
 
 namespace ps {
 
+constexpr int kK1Block = 256;  // splats per K1 / K3 CTA
+constexpr int kWinCap = 1024;  // tile cells of a CTA's shared window (K1 counts, K3 scatters)
 constexpr int kShPlanes = 12; // 48 floats = 16 coefficients x 3 channels, as float4
 
 
@@ -89,6 +91,11 @@ struct FrameDev {
     uint2* ranges = nullptr;            // per tile [start, end)
     uint32_t* big_tiles = nullptr;      // ids of tiles with > 1024 pairs
     uint32_t* tile_order = nullptr;     // tile ids, longest bucket first (K2; the blend's CTA -> tile map)
+    // K1's per-CTA tile windows (kK1Block splats per CTA): window rect (x0, y0,
+    // w, h; w = 0: no window) and its per-tile pair counts (stride kWinCap), so
+    // K3 scatters without counting again
+    int4* win_rect = nullptr;
+    uint32_t* win_counts = nullptr;
     uint32_t* tile_count = nullptr;     // pairs per tile (K1a), then the K3 bucket cursors
     uint32_t* flags = nullptr;          // flagged pixel ids (capacity W*H)
     double4* replay_vals = nullptr;     // exact fp64 (r, g, b, T) per flagged pixel (optional)

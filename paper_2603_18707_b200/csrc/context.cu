@@ -255,6 +255,8 @@ size_t frame_bytes(int64_t n) {
     s += 3 * al(16 * n);                                 // mean2d, conic_ab, conic_cq
     s += al(8 * n) + al(8 * n) + al(8 * n);              // rect, opacity_eff, tmask
     s += 2 * al(16 * n) + al(8 * n);                     // bl0, bl1, bl2
+    const size_t nblk = static_cast<size_t>((n + kK1Block - 1) / kK1Block);
+    s += al(16 * nblk) + al(4 * nblk * kWinCap);         // win_rect, win_counts
     return s;
 }
 
@@ -281,6 +283,11 @@ int ensure_frame(ps_ctx* c, int64_t n) {
     c->f.bl0 = carve<float4>(p, cap);
     c->f.bl1 = carve<float4>(p, cap);
     c->f.bl2 = carve<float2>(p, cap);
+    {
+        const int64_t nblk = (cap + kK1Block - 1) / kK1Block;
+        c->f.win_rect = carve<int4>(p, nblk);
+        c->f.win_counts = carve<uint32_t>(p, nblk * kWinCap);
+    }
     size_t rs = radix_scratch_bytes(cap);
     size_t ss = scan_scratch_bytes(cap);
     if (rs > c->radix_scratch_size) {

@@ -499,7 +499,6 @@ __device__ __forceinline__ unsigned long long warp_tight_tests(ScreenRec* srec, 
 // in a shared-memory window over the union of the CTA's tile rects, and only
 // one global atomic per distinct tile per CTA is issued. Rects of > 64 tiles
 // (or a window larger than kWinCap) fall back to direct global atomics.
-constexpr int kWinCap = 1024;
 
 struct Window {
     int x0, y0, w, h;
@@ -731,8 +730,13 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                 }
             }
             __syncthreads();
-            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x)
-                if (win[k]) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], win[k]);
+            uint32_t* wc = f.win_counts + static_cast<size_t>(blockIdx.x) * kWinCap; // for K3
+            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) {
+                const uint32_t v = win[k];
+                wc[k] = v;
+                if (v) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], v);
+            }
+            if (threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(W.x0, W.y0, W.w, W.h);
         } else if (small) {
             unsigned long long m = my_mask;
             while (m) {
@@ -741,6 +745,7 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
                 atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
             }
         }
+        if (!W.ok && threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1078,7 +1083,6 @@ __device__ __noinline__ void build_tile_order(const uint2* __restrict__ ranges, 
 __global__ void __launch_bounds__(256, 6) k_duplicate_buckets(FrameDev f, FrameParams P, int64_t n,
                                                                const DevCounters* __restrict__ ctr) {
     __shared__ uint32_t win[kWinCap];
-    __shared__ int wb[4];
     pdl_trigger(); // the blend / long sorts may be scheduled into freed slots
     pdl_wait();    // K2's cursors and key range
     if (pairs_overflow(f)) return; // speculative frame over capacity: re-run by the host
@@ -1114,21 +1118,20 @@ __global__ void __launch_bounds__(256, 6) k_duplicate_buckets(FrameDev f, FrameP
                           P.tiles_x, static_cast<uint32_t>(i), r[0], r[1], r[2], r[3]);
         }
     }
-    const Window W = block_window(small, r, wb);
+    // the same CTA of K1 counted this window's pairs (geometry_view): reserve
+    // each cell's bucket slots from those counts (one global atomic per cell)
+    const int4 wr = f.win_rect[blk];
+    Window W;
+    W.x0 = wr.x; W.y0 = wr.y; W.w = wr.z; W.h = wr.w;
+    W.ok = wr.z > 0;
     if (W.ok) {
-        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) win[k] = 0;
-        __syncthreads();
-        unsigned long long m = m0;
-        while (m) {
-            const int b = __ffsll(static_cast<long long>(m)) - 1;
-            m &= m - 1;
-            atomicAdd(&win[rect_bit_win(r, b, W)], 1u);
+        const uint32_t* wc = f.win_counts + static_cast<size_t>(blk) * kWinCap;
+        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) {
+            const uint32_t v = wc[k];
+            win[k] = v ? atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], v) : 0u;
         }
         __syncthreads();
-        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x)
-            if (win[k]) win[k] = atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], win[k]);
-        __syncthreads();
-        m = m0;
+        unsigned long long m = m0;
         while (m) {
             const int b = __ffsll(static_cast<long long>(m)) - 1;
             m &= m - 1;
