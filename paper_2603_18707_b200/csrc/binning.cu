@@ -18,37 +18,49 @@ namespace ps {
 namespace {
 
 constexpr int kScanThreads = 1024;
-constexpr int kScanPer = 16; // consecutive tiles per thread per round (16K tiles per round)
+constexpr int kScanPer = 8;                            // tiles per thread per round
+constexpr int kScanRound = kScanThreads * kScanPer;    // 8192 tiles: a 1080p frame is one round
+__host__ __device__ constexpr int scan_pad(int i) { return i + (i >> 5); } // conflict-free blocked reads
 
 // One CTA: exclusive scan of the per-tile pair counts into ranges and K3
 // cursors, the total / longest bucket, and the list of buckets > list_min (sorted
-// outside the blend). Each thread owns 16 consecutive tiles (vector loads and
-// stores), so a 1080p frame (8160 tiles) is one round.
+// outside the blend). Global memory is read and written in striped order (each
+// warp instruction one or two whole 128-byte lines) and transposed through
+// shared memory to the blocked order of the scan (thread t owns tiles
+// 8t .. 8t + 7 of the round): one SM's load/store path carries the whole
+// kernel, so uncoalesced per-thread runs of 16 tiles had made it
+// transaction-bound (8 us at 1080p, 22 us at 4K).
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict__ count, uint2* __restrict__ ranges,
                                                             int n_tiles, DevCounters* ctr, uint32_t* __restrict__ big_list,
                                                             uint32_t list_min) {
+    __shared__ uint32_t sc[scan_pad(kScanRound) + 1];
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t wmax[32];
     pdl_trigger(); // K3 may be scheduled now (it waits for this scan)
     pdl_wait();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     uint32_t carry = 0, mx = 0;
-    for (int base = 0; base < n_tiles; base += kScanThreads * kScanPer) {
-        const int t0 = base + threadIdx.x * kScanPer;
-        uint32_t v[kScanPer];
-        if (t0 + kScanPer <= n_tiles) {
+    uint32_t nxt[kScanPer]; // this round's counts, loaded during the previous round
 #pragma unroll
-            for (int q = 0; q < kScanPer; q += 4) {
-                const uint4 x = *reinterpret_cast<const uint4*>(count + t0 + q);
-                v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
-            }
-        } else {
+    for (int q = 0; q < kScanPer; ++q) nxt[q] = q * kScanThreads + t < n_tiles ? count[q * kScanThreads + t] : 0u;
+    for (int base = 0; base < n_tiles; base += kScanRound) {
+        const int cnt = min(kScanRound, n_tiles - base);
 #pragma unroll
-            for (int q = 0; q < kScanPer; ++q) v[q] = t0 + q < n_tiles ? count[t0 + q] : 0u;
+        for (int q = 0; q < kScanPer; ++q) sc[scan_pad(q * kScanThreads + t)] = nxt[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) { // the next round's loads overlap this round
+            const int g = base + kScanRound + q * kScanThreads + t;
+            nxt[q] = g < n_tiles ? count[g] : 0u;
         }
+        uint32_t v[kScanPer];
         uint32_t sum = 0;
 #pragma unroll
-        for (int q = 0; q < kScanPer; ++q) { sum += v[q]; mx = max(mx, v[q]); }
+        for (int q = 0; q < kScanPer; ++q) {
+            v[q] = sc[scan_pad(t * kScanPer + q)];
+            sum += v[q];
+            mx = max(mx, v[q]);
+        }
         uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -68,34 +80,27 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(uint32_t* __restrict
         }
         __syncthreads();
         uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - sum;
-        if (t0 + kScanPer <= n_tiles) {
-            uint32_t cur[kScanPer];
 #pragma unroll
-            for (int q = 0; q < kScanPer; ++q) {
-                cur[q] = excl;
-                if (v[q] > list_min) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t0 + q);
-                excl += v[q];
-            }
+        for (int q = 0; q < kScanPer; ++q) {
+            const int i = t * kScanPer + q;
+            if (v[q] > list_min && i < cnt) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(base + i);
+            sc[scan_pad(i)] = excl;
+            excl += v[q];
+        }
+        const uint32_t next = carry + wsum[31];
+        if (t == 0) sc[scan_pad(kScanRound)] = next; // the round's end (padding tiles hold 0)
+        __syncthreads();
 #pragma unroll
-            for (int q = 0; q < kScanPer; q += 2)
-                *reinterpret_cast<uint4*>(ranges + t0 + q) = make_uint4(cur[q], cur[q] + v[q], cur[q + 1], cur[q + 1] + v[q + 1]);
-#pragma unroll
-            for (int q = 0; q < kScanPer; q += 4) // the cursors for K3
-                *reinterpret_cast<uint4*>(count + t0 + q) = make_uint4(cur[q], cur[q + 1], cur[q + 2], cur[q + 3]);
-        } else {
-#pragma unroll
-            for (int q = 0; q < kScanPer; ++q) {
-                const int t = t0 + q;
-                if (t < n_tiles) {
-                    ranges[t] = make_uint2(excl, excl + v[q]);
-                    count[t] = excl;
-                    if (v[q] > list_min) big_list[atomicAdd(&ctr->big_tiles, 1u)] = static_cast<uint32_t>(t);
-                }
-                excl += v[q];
+        for (int q = 0; q < kScanPer; ++q) {
+            const int i = q * kScanThreads + t;
+            if (i < cnt) {
+                const uint32_t e = sc[scan_pad(i)];
+                ranges[base + i] = make_uint2(e, sc[scan_pad(i + 1)]);
+                count[base + i] = e; // the cursors for K3
             }
         }
-        carry += wsum[31];
-        __syncthreads();
+        carry = next;
+        __syncthreads(); // sc and wsum are reused by the next round
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
