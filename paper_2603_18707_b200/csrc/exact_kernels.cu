@@ -549,6 +549,9 @@ __device__ __forceinline__ int rect_bit_win(const int r[4], int b, const Window&
 //       tile_rect (raster.cpp:71-86) and the tight-tile bitmask (raster.cpp:126-128).
 //   K1b k_shade<BK>: SH colour (projection.cpp:93-116) + the fp32 blend record,
 //       specialised on the blend kernel.
+#ifndef PS_K1_LATE_WINDOW
+#define PS_K1_LATE_WINDOW 0
+#endif
 enum BoundClass : int { kBcStp = 0, kBcZero = 1, kBcOaExp = 2, kBcOaP1 = 3, kBcOaP2 = 4, kBcOaP3 = 5, kBcGeneric = 6 };
 
 // culling_bound_for specialised per class. 1 = bound set, 0 = nullopt (below
@@ -613,12 +616,49 @@ struct GeoOut {
     double x = 0.0;                             // the culling root (bound_for)
 };
 
+// Tight pairs per tile for the bucket scan (K2), aggregated in the CTA's
+// shared window (block_window); every thread of the CTA calls this.
+__device__ __forceinline__ void tile_window_counts(bool small, const int (&my_r)[4], unsigned long long my_mask,
+                                                   const FrameDev& f, const FrameParams& P) {
+    __shared__ uint32_t win[kWinCap];
+    __shared__ int wb[4];
+    const Window W = block_window(small, my_r, wb);
+    if (W.ok) {
+        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) win[k] = 0;
+        __syncthreads();
+        if (small) {
+            unsigned long long m = my_mask;
+            while (m) {
+                const int b = __ffsll(static_cast<long long>(m)) - 1;
+                m &= m - 1;
+                atomicAdd(&win[rect_bit_win(my_r, b, W)], 1u);
+            }
+        }
+        __syncthreads();
+        uint32_t* wc = f.win_counts + static_cast<size_t>(blockIdx.x) * kWinCap; // for K3
+        for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) {
+            const uint32_t v = win[k];
+            wc[k] = v;
+            if (v) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], v);
+        }
+        if (threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(W.x0, W.y0, W.w, W.h);
+    } else if (small) {
+        unsigned long long m = my_mask;
+        while (m) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
+        }
+    }
+    if (!W.ok && threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
+}
+
 // CTA_RED: the frame counters are reduced over the CTA before their atomics
 // (one update per CTA instead of per warp; see the end).
 template <int BC, bool CTA_RED = false>
 __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
                                               double opacity, const FrameParams& P, const FrameDev& f,
-                                              DevCounters* ctr, GeoOut* out = nullptr) {
+                                              DevCounters* ctr, GeoOut* out = nullptr, ulonglong2* late = nullptr) {
     __shared__ ScreenRec srec[256];
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
@@ -715,37 +755,12 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
         if (in) f.tcount[i] = static_cast<uint32_t>(tight);
     }
     if (f.tile_count) { // tight pairs per tile for the bucket scan (K2)
-        __shared__ uint32_t win[kWinCap];
-        __shared__ int wb[4];
-        const Window W = block_window(small, my_r, wb);
-        if (W.ok) {
-            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) win[k] = 0;
-            __syncthreads();
-            if (small) {
-                unsigned long long m = my_mask;
-                while (m) {
-                    const int b = __ffsll(static_cast<long long>(m)) - 1;
-                    m &= m - 1;
-                    atomicAdd(&win[rect_bit_win(my_r, b, W)], 1u);
-                }
-            }
-            __syncthreads();
-            uint32_t* wc = f.win_counts + static_cast<size_t>(blockIdx.x) * kWinCap; // for K3
-            for (int k = threadIdx.x; k < W.w * W.h; k += blockDim.x) {
-                const uint32_t v = win[k];
-                wc[k] = v;
-                if (v) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], v);
-            }
-            if (threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(W.x0, W.y0, W.w, W.h);
-        } else if (small) {
-            unsigned long long m = my_mask;
-            while (m) {
-                const int b = __ffsll(static_cast<long long>(m)) - 1;
-                m &= m - 1;
-                atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
-            }
-        }
-        if (!W.ok && threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
+        if (late) late[threadIdx.x] = make_ulonglong2(small ? my_mask : 0ull,
+                                                      (static_cast<unsigned long long>(static_cast<uint16_t>(my_r[0]))) |
+                                                      (static_cast<unsigned long long>(static_cast<uint16_t>(my_r[1])) << 16) |
+                                                      (static_cast<unsigned long long>(static_cast<uint16_t>(my_r[2])) << 32) |
+                                                      (static_cast<unsigned long long>(static_cast<uint16_t>(my_r[3])) << 48));
+        else tile_window_counts(small, my_r, my_mask, f, P);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -905,14 +920,31 @@ __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParam
         opacity = s.opacity[i];
     }
     GeoOut g;
+#if PS_K1_LATE_WINDOW
+    // the CTA-wide window counting after the shading: no CTA barrier between a
+    // warp's fp64 geometry and its SH stream
+    __shared__ ulonglong2 s_late[256];
+    geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g, s_late);
+#else
     geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g);
     pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
+#endif
     if (g.visible) {
         float v[48];
         load_sh<1>(s, i, P.sh_floats4, v);
         const bool same = kThresholdIsBound<BC, BK> && !P.cfg.has_culling_kernel;
         shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o, same ? &g.x : nullptr);
     }
+#if PS_K1_LATE_WINDOW
+    if (f.tile_count) {
+        const ulonglong2 wm = s_late[threadIdx.x];
+        const int r[4] = {static_cast<int>(wm.y & 0xffffu), static_cast<int>((wm.y >> 16) & 0xffffu),
+                          static_cast<int>(static_cast<int16_t>((wm.y >> 32) & 0xffffu)),
+                          static_cast<int>(static_cast<int16_t>(wm.y >> 48))};
+        tile_window_counts(wm.x != 0ull, r, wm.x, f, P);
+    }
+    pdl_trigger();
+#endif
 }
 
 // Multi-view K1b: the splat's SH coefficients (192 B, most of K1b's traffic)
