@@ -549,9 +549,6 @@ __device__ __forceinline__ int rect_bit_win(const int r[4], int b, const Window&
 //       tile_rect (raster.cpp:71-86) and the tight-tile bitmask (raster.cpp:126-128).
 //   K1b k_shade<BK>: SH colour (projection.cpp:93-116) + the fp32 blend record,
 //       specialised on the blend kernel.
-#ifndef PS_K1_LATE_WINDOW
-#define PS_K1_LATE_WINDOW 0
-#endif
 enum BoundClass : int { kBcStp = 0, kBcZero = 1, kBcOaExp = 2, kBcOaP1 = 3, kBcOaP2 = 4, kBcOaP3 = 5, kBcGeneric = 6 };
 
 // culling_bound_for specialised per class. 1 = bound set, 0 = nullopt (below
@@ -653,12 +650,31 @@ __device__ __forceinline__ void tile_window_counts(bool small, const int (&my_r)
     if (!W.ok && threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
 }
 
+// The CTA's six frame counters (per-warp partials in red[k][warp], written
+// before a CTA barrier) into the device counters: one atomic each per CTA.
+__device__ __forceinline__ void flush_cta_counters(const unsigned long long (*red)[8], DevCounters* ctr) {
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x, nw = blockDim.x >> 5;
+        unsigned long long v = red[k][0];
+        for (int j = 1; j < nw; ++j) v = k < 2 ? max(v, red[k][j]) : v + red[k][j];
+        if (v) {
+            if (k == 0) atomicMax(&ctr->key_min, v);
+            else if (k == 1) atomicMax(&ctr->key_max, v);
+            else if (k == 2) atomicAdd(&ctr->frustum, v);
+            else if (k == 3) atomicAdd(&ctr->coarse, v);
+            else if (k == 4) atomicAdd(&ctr->tight, v);
+            else atomicAdd(&ctr->visible, v);
+        }
+    }
+}
+
 // CTA_RED: the frame counters are reduced over the CTA before their atomics
 // (one update per CTA instead of per warp; see the end).
 template <int BC, bool CTA_RED = false>
 __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (&mean)[3], const double (&c6)[6],
                                               double opacity, const FrameParams& P, const FrameDev& f,
-                                              DevCounters* ctr, GeoOut* out = nullptr, ulonglong2* late = nullptr) {
+                                              DevCounters* ctr, GeoOut* out = nullptr, ulonglong2* late = nullptr,
+                                              unsigned long long (*late_red)[8] = nullptr) {
     __shared__ ScreenRec srec[256];
     unsigned long long frustum = 0, coarse = 0, tight = 0, visible = 0;
     unsigned long long kmin_inv = 0ull, kmax = 0ull; // min tracked as max of the complement
@@ -789,26 +805,16 @@ __device__ __forceinline__ void geometry_view(int64_t i, bool in, const double (
     // ~190k updates per address per frame) they throttled the fused K1 at scale
     // (C3 preprocess 1,437 -> 870 us, C4 707 -> 405 us with this; at 1M the
     // per-warp atomics are as fast and the split kernels slower with it)
-    __shared__ unsigned long long s_red[6][8];
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ unsigned long long s_red_own[6][8];
+    unsigned long long (*s_red)[8] = late_red ? late_red : s_red_own;
+    const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         s_red[0][w] = kmin_inv; s_red[1][w] = kmax; s_red[2][w] = frustum;
         s_red[3][w] = coarse; s_red[4][w] = tight; s_red[5][w] = visible;
     }
+    if (late_red) return; // flushed by the caller after its next CTA barrier
     __syncthreads();
-    if (threadIdx.x < 6) {
-        const int k = threadIdx.x;
-        unsigned long long v = s_red[k][0];
-        for (int j = 1; j < nw; ++j) v = k < 2 ? max(v, s_red[k][j]) : v + s_red[k][j];
-        if (v) {
-            if (k == 0) atomicMax(&ctr->key_min, v);
-            else if (k == 1) atomicMax(&ctr->key_max, v);
-            else if (k == 2) atomicAdd(&ctr->frustum, v);
-            else if (k == 3) atomicAdd(&ctr->coarse, v);
-            else if (k == 4) atomicAdd(&ctr->tight, v);
-            else atomicAdd(&ctr->visible, v);
-        }
-    }
+    flush_cta_counters(s_red, ctr);
 }
 
 template <int BC>
@@ -920,31 +926,30 @@ __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParam
         opacity = s.opacity[i];
     }
     GeoOut g;
-#if PS_K1_LATE_WINDOW
-    // the CTA-wide window counting after the shading: no CTA barrier between a
-    // warp's fp64 geometry and its SH stream
+    // The CTA-wide steps (the tile window counts for K2 / K3 and, with
+    // CTA_RED, the counter flush) run after the shading: no CTA barrier between
+    // a warp's fp64 geometry and its SH stream (C2 -3 us, C3 -13 us, exp -8 us
+    // against counting before the shading).
     __shared__ ulonglong2 s_late[256];
-    geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g, s_late);
-#else
-    geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g);
-    pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
-#endif
+    __shared__ unsigned long long s_red[6][8];
+    geometry_view<BC, CTA_RED>(i, in, mean, c6, opacity, P, f, ctr, &g, s_late, CTA_RED ? s_red : nullptr);
     if (g.visible) {
         float v[48];
         load_sh<1>(s, i, P.sh_floats4, v);
         const bool same = kThresholdIsBound<BC, BK> && !P.cfg.has_culling_kernel;
         shade_record<BK>(i, mean, v, P, f, g.a, g.b, g.c, g.o, same ? &g.x : nullptr);
     }
-#if PS_K1_LATE_WINDOW
     if (f.tile_count) {
         const ulonglong2 wm = s_late[threadIdx.x];
         const int r[4] = {static_cast<int>(wm.y & 0xffffu), static_cast<int>((wm.y >> 16) & 0xffffu),
                           static_cast<int>(static_cast<int16_t>((wm.y >> 32) & 0xffffu)),
                           static_cast<int>(static_cast<int16_t>(wm.y >> 48))};
-        tile_window_counts(wm.x != 0ull, r, wm.x, f, P);
+        tile_window_counts(wm.x != 0ull, r, wm.x, f, P); // (its CTA barriers order s_red too)
+    } else if (CTA_RED) {
+        __syncthreads();
     }
-    pdl_trigger();
-#endif
+    if (CTA_RED) flush_cta_counters(s_red, ctr);
+    pdl_trigger(); // K2 may be scheduled once every CTA is past its tile counts
 }
 
 // Multi-view K1b: the splat's SH coefficients (192 B, most of K1b's traffic)
