@@ -639,15 +639,20 @@ __device__ __forceinline__ void tile_window_counts(bool small, const int (&my_r)
             if (v) atomicAdd(&f.tile_count[(W.y0 + k / W.w) * P.tiles_x + W.x0 + k % W.w], v);
         }
         if (threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(W.x0, W.y0, W.w, W.h);
-    } else if (small) {
-        unsigned long long m = my_mask;
-        while (m) {
-            const int b = __ffsll(static_cast<long long>(m)) - 1;
-            m &= m - 1;
-            atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
+    } else {
+        if (small) {
+            unsigned long long m = my_mask;
+            while (m) {
+                const int b = __ffsll(static_cast<long long>(m)) - 1;
+                m &= m - 1;
+                atomicAdd(&f.tile_count[rect_bit_tile(my_r, b, P.tiles_x)], 1u);
+            }
         }
+        if (threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
+        // (W.ok is CTA-uniform) every thread has read wb before a next call's
+        // thread 0 resets it (the multi-view kernels count view after view)
+        __syncthreads();
     }
-    if (!W.ok && threadIdx.x == 0) f.win_rect[blockIdx.x] = make_int4(0, 0, 0, 0);
 }
 
 // The CTA's six frame counters (per-warp partials in red[k][warp], written
