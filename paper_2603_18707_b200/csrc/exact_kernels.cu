@@ -1303,7 +1303,10 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
     // reduced per CTA (geometry_view CTA_RED): with per-warp counter atomics the
     // fused kernel lost to the split ones at scale (C3 1,437 vs 1,027 us),
     // with per-CTA ones it wins there too (870 us)
-    constexpr int64_t kFusedWarpCounters = 1500000;
+#ifndef PS_FUSED_WARP_COUNTERS
+#define PS_FUSED_WARP_COUNTERS 1500000 // (0: per-CTA counters at every size; sanitizer builds)
+#endif
+    constexpr int64_t kFusedWarpCounters = PS_FUSED_WARP_COUNTERS;
 #define PS_FUSED(BCV, BKV)                                                                 \
     if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
         if (s.n <= kFusedWarpCounters)                                                   \
