@@ -946,9 +946,10 @@ __global__ void __launch_bounds__(256, MINB) k_preprocess(SceneDev s, FrameParam
     }
     if (f.tile_count) {
         const ulonglong2 wm = s_late[threadIdx.x];
+        // (the rect is read only for a nonzero mask, i.e. a visible small rect:
+        // tile indices < 2^16 like f.rect's)
         const int r[4] = {static_cast<int>(wm.y & 0xffffu), static_cast<int>((wm.y >> 16) & 0xffffu),
-                          static_cast<int>(static_cast<int16_t>((wm.y >> 32) & 0xffffu)),
-                          static_cast<int>(static_cast<int16_t>(wm.y >> 48))};
+                          static_cast<int>((wm.y >> 32) & 0xffffu), static_cast<int>(wm.y >> 48)};
         tile_window_counts(wm.x != 0ull, r, wm.x, f, P); // (its CTA barriers order s_red too)
     } else if (CTA_RED) {
         __syncthreads();
@@ -1303,6 +1304,9 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
     // reduced per CTA (geometry_view CTA_RED): with per-warp counter atomics the
     // fused kernel lost to the split ones at scale (C3 1,437 vs 1,027 us),
     // with per-CTA ones it wins there too (870 us)
+#ifndef PS_K1_MINB
+#define PS_K1_MINB 3
+#endif
 #ifndef PS_FUSED_WARP_COUNTERS
 #define PS_FUSED_WARP_COUNTERS 1500000 // (0: per-CTA counters at every size; sanitizer builds)
 #endif
@@ -1310,9 +1314,9 @@ int launch_preprocess(const SceneDev& s, const FrameParams& P, const FrameDev& f
 #define PS_FUSED(BCV, BKV)                                                                 \
     if (P.bound_class == BCV && P.blend_class == BKV) {                                  \
         if (s.n <= kFusedWarpCounters)                                                   \
-            k_preprocess<BCV, BKV, 3, false><<<blocks, 256, 0, st>>>(s, P, f, ctr);      \
+            k_preprocess<BCV, BKV, PS_K1_MINB, false><<<blocks, 256, 0, st>>>(s, P, f, ctr);      \
         else                                                                             \
-            k_preprocess<BCV, BKV, 3, true><<<blocks, 256, 0, st>>>(s, P, f, ctr);       \
+            k_preprocess<BCV, BKV, PS_K1_MINB, true><<<blocks, 256, 0, st>>>(s, P, f, ctr);       \
         return 1;                                                                        \
     }
     PS_FUSED(kBcStp, kBkExp)
